@@ -1,0 +1,160 @@
+/*
+ * specache.h -- C ABI of the B200-native SpeCache decode hot path.
+ *
+ * The reference (SpeCache, arXiv 2503.16163; /root/reference/pkg/src/speckv)
+ * has no FFI: its boundary is the Python object API of TwoTierCache and the
+ * per-layer body of SpeculativeDecoder.  Each entry point below replaces one
+ * piece of that API (file:line relative to pkg/src/speckv).  Plain pointers
+ * and sizes only: device pointers are CUDA device addresses, `stream` is a
+ * cudaStream_t passed as void*.  No exceptions cross this boundary; every
+ * function returns an spc_status (0 = ok).  The Python binding
+ * (paper_2503_16163_b200/_lib.py) maps SPC_EINVAL -> ValueError and
+ * SPC_EPROTO -> ProtocolError, matching the reference's error convention
+ * (kvcache.py:40-44,156-157,202-209; transfer.py:31-32,86-87,98-99).
+ *
+ * Data types: rows / queries / outputs are bf16 (uint16 bit patterns),
+ * accumulation is fp32, quantizer parameters are exact fp64 functions of the
+ * group's bf16 (min, max) which the cache stores.
+ */
+#ifndef SPECACHE_H_
+#define SPECACHE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPC_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SPC_API __attribute__((visibility("default")))
+#else
+#define SPC_API
+#endif
+
+typedef enum spc_status {
+  SPC_OK = 0,
+  SPC_EINVAL = -22,  /* ValueError in the reference                          */
+  SPC_EPROTO = -71,  /* ProtocolError (phase / ticket misuse)                 */
+  SPC_ENOMEM = -12,  /* device or pinned-host allocation failed               */
+  SPC_ECUDA = -5     /* CUDA runtime error (message in spc_last_error())      */
+} spc_status;
+
+typedef enum spc_topk_scope {
+  SPC_SCOPE_LAYER = 0,   /* reference: one set per (seq, layer), agg over all q heads (engine.py:317) */
+  SPC_SCOPE_KV_HEAD = 1  /* north-star extension: one set per (seq, layer, kv head)                    */
+} spc_topk_scope;
+
+/* Cache geometry; replaces CacheBudget (kvcache.py:29-44) + the TwoTierCache
+ * constructor arguments (kvcache.py:116-118), batched over `batch` sequences
+ * that advance in lockstep. */
+typedef struct spc_dims {
+  int32_t layers;
+  int32_t batch;
+  int32_t kv_heads;
+  int32_t q_heads;
+  int32_t head_dim;
+  int32_t bits;            /* 1, 2, 4 or 16 (kvcache.py:25-26)               */
+  int32_t group_size;      /* g                                              */
+  int32_t residual;        /* r                                              */
+  int32_t prefetch_k;      /* k                                              */
+  int32_t context_length;  /* L: per-sequence capacity in positions          */
+  int32_t topk_scope;      /* spc_topk_scope                                 */
+  int32_t host_layers;     /* distinct pinned-host slow-tier slabs; layer l uses
+                              slab l % host_layers (0 -> layers).  Aliased layers
+                              must be fed identical KV.                       */
+} spc_dims;
+
+typedef struct spc_cache spc_cache;
+
+/* -- library -------------------------------------------------------------- */
+SPC_API int spc_abi_version(void);
+/* Message for the last non-OK status on this thread. */
+SPC_API const char* spc_last_error(void);
+
+/* -- construction: TwoTierCache.__init__ (kvcache.py:116-129) --------------- */
+SPC_API int spc_cache_create(const spc_dims* dims, int device, spc_cache** out);
+SPC_API int spc_cache_destroy(spc_cache* cache);
+/* 1 when the tensor-core fast path serves this geometry (d=128, g=32, bits 1/2). */
+SPC_API int spc_cache_fast_path(const spc_cache* cache);
+/* Attention implementation: 0 auto (fast when supported), 1 generic exact, 2 fast (error if unsupported). */
+SPC_API int spc_set_attend_impl(spc_cache* cache, int impl);
+SPC_API int64_t spc_device_bytes(const spc_cache* cache);
+SPC_API int64_t spc_host_bytes(const spc_cache* cache);
+
+/* -- bookkeeping: length / quantized_frontier / row_bytes (kvcache.py:133-150) */
+SPC_API int64_t spc_length(const spc_cache* cache, int layer);
+SPC_API int64_t spc_frontier(const spc_cache* cache, int layer);
+SPC_API int64_t spc_row_bytes(const spc_cache* cache, int64_t positions);
+
+/* -- writes ----------------------------------------------------------------- */
+/* Bulk prefill of an empty layer: equivalent to n x append_verified
+ * (kvcache.py:162-171, called at engine.py:234-235).  K, V: device bf16
+ * [batch][n][kv_heads][head_dim].  Writes the slow tier (pinned host),
+ * quantizes [0, f(n)) and stores the residual window [f(n), n). */
+SPC_API int spc_prefill(spc_cache* cache, int layer, const void* K, const void* V, int n, void* stream);
+/* append_verified (kvcache.py:162-171): one row per sequence.  k_rows, v_rows:
+ * device bf16 [batch][kv_heads][head_dim] at element stride `seq_stride`
+ * between sequences (0 -> kv_heads*head_dim).  Migrates when the residual
+ * reaches r+g (migrate_residual, kvcache.py:173-192). */
+SPC_API int spc_append(spc_cache* cache, int layer, const void* k_rows, const void* v_rows,
+               int64_t seq_stride, void* stream);
+/* migrate_residual (kvcache.py:173-192): quantize the oldest g residual rows;
+ * SPC_EINVAL when fewer than g are resident. */
+SPC_API int spc_migrate(spc_cache* cache, int layer, void* stream);
+/* pin (kvcache.py:194-218) for one (seq, unit): replaces the pinned set.
+ * positions: HOST int32 [npos]; rows default to a slow-tier fetch when
+ * k_rows/v_rows are NULL, else device bf16 [npos][heads_per_unit][head_dim]. */
+SPC_API int spc_pin(spc_cache* cache, int layer, int seq, int unit, const int32_t* positions,
+            int npos, const void* k_rows, const void* v_rows, void* stream);
+
+/* -- the hot path ------------------------------------------------------------ */
+/* Pre-decoding (engine.py:245-268): q device bf16 [batch][1][q_heads][d],
+ * k_new/v_new [batch][1][kv_heads][d].  out: device bf16 [batch][1][q_heads][d].
+ * Issues ticket (step 0, layer) -- top-k + prefetch on the cache's copy stream. */
+SPC_API int spc_predecode_layer(spc_cache* cache, int layer, const void* q, const void* k_new,
+                        const void* v_new, void* out, void* stream);
+/* Dual-token decode step, one layer (engine.py:299-321): awaits ticket
+ * (step-1, layer) (transfer.py:96-100 -> cudaStreamWaitEvent), attends rows
+ * 0 (verified) and 1 (speculative) over packed + pinned + residual + in-step
+ * rows, writes out [batch][2][q_heads][d] bf16 and pinned_mass [batch][q_heads]
+ * fp32 (device), issues ticket (step, layer) and appends row 0. */
+SPC_API int spc_decode_layer(spc_cache* cache, int layer, int step, const void* q, const void* k_new,
+                     const void* v_new, void* out, float* pinned_mass, void* stream);
+/* The last ticket of `layer` (PrefetchTicket, transfer.py:50-55): picked
+ * positions device int32 [batch][units][k] (-1 padded, ascending) and new-pin
+ * counts device int32 [batch][units].  Ordered after the selection on `stream`. */
+SPC_API int spc_ticket(spc_cache* cache, int layer, int32_t* picked, int32_t* new_count, void* stream);
+/* select_topk (engine.py:75-84) over eligible [0, n): device fp32 scores (>= 0),
+ * device int32 out[k] ascending, -1 padded; ties to the lower position. */
+SPC_API int spc_select_topk(const float* scores, int n, int k, int32_t* out, void* stream);
+/* Debug: speculative-row aggregate of `layer`, device fp32 [batch][units][context_length]. */
+SPC_API int spc_debug_agg(spc_cache* cache, int layer, float* agg, void* stream);
+
+/* -- reads / parity ------------------------------------------------------------ */
+/* materialize (kvcache.py:222-243) for one (seq, head): device fp32 [n][d] x2,
+ * bit-identical to the reference's float32 dequantization. */
+SPC_API int spc_materialize(spc_cache* cache, int layer, int seq, int head, float* keys, float* values,
+                    void* stream);
+/* Normative fast-tier export (snapshot(), kvcache.py:270-281 / quant.py:150-160)
+ * for one (layer, seq), device buffers:
+ *   key_codes uint8 [f/g][H][d][nb], key_zero/key_scale fp16 bits [f/g][H][d]
+ *   val_codes uint8 [f][H][nchunk][nb], val_zero/val_scale fp16 bits [f][H][nchunk]
+ * nb = ceil(g*bits/8), nchunk = ceil(d/g). */
+SPC_API int spc_export_packed(spc_cache* cache, int layer, int seq, uint8_t* key_codes,
+                      uint16_t* key_zero, uint16_t* key_scale, uint8_t* val_codes,
+                      uint16_t* val_zero, uint16_t* val_scale, void* stream);
+/* slow_fetch (kvcache.py:245-259) from the pinned host tier: HOST int32
+ * positions, HOST bf16 outputs [npos][kv_heads][d].  Synchronous. */
+SPC_API int spc_slow_fetch(spc_cache* cache, int layer, int seq, const int32_t* positions, int npos,
+                   void* k_out, void* v_out);
+/* Device pointer + element count of the pin state of (layer): pin_pos int32
+ * [batch][units][k] (-1 = empty slot). */
+SPC_API int spc_pin_state(spc_cache* cache, int layer, const int32_t** pin_pos);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECACHE_H_ */

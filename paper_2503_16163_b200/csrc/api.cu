@@ -1,0 +1,526 @@
+// api.cu -- the C ABI (include/specache.h): cache object, allocation, streams,
+// per-layer ticket protocol, and the K1..K6 launch sequence of one decode layer.
+//
+// Stream structure per layer l (SURVEY.md 8(b) "Threading"):
+//   compute stream : [wait ev_pf(l)] K2 attend -> K3 combine -> K3 agg
+//                    -> record ev_agg(l) -> K6 append (+K1 migration)
+//   copy stream    : [wait ev_agg(l)] K4 top-k + pin diff -> K5 prefetch
+//                    -> record ev_pf(l)
+// so the selection and the PCIe gather for step t+1 overlap the compute of the
+// following layers; decode_layer(l, t+1) waits on ev_pf(l) -- the device form
+// of SimulatedChannel.await_layer (transfer.py:96-100).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/specache.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace spc;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CUDA_TRY(expr)                                                               \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return fail(SPC_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));    \
+  } while (0)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+int64_t frontier_of(int64_t n, int r, int g) { return n < r ? 0 : (int64_t)g * ((n - r) / g); }
+constexpr int kSplitCap = 128;
+constexpr int kNumSMs = 148;
+}  // namespace
+
+struct spc_cache {
+  Geo G{};
+  int device = 0;
+  int impl = 0;  // 0 auto, 1 generic exact, 2 fast
+  std::vector<LayerBufs> L;
+  std::vector<void*> dev_allocs;
+  __nv_bfloat16* host_k = nullptr;
+  __nv_bfloat16* host_v = nullptr;
+  size_t host_bytes = 0, dev_bytes = 0, slab_elems = 0;
+  std::vector<int64_t> n, f;
+  std::vector<int> ticket;  // pending ticket step per layer (-1 none)
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> ev_agg, ev_pf;
+  float *part_o = nullptr, *part_ml = nullptr, *pin_ml = nullptr, *spill = nullptr, *mz = nullptr;
+  int32_t* staging = nullptr;
+  int context_length = 0;
+};
+
+namespace {
+int dalloc(spc_cache* c, void** p, size_t bytes) {
+  bytes = std::max<size_t>(bytes, 256);
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess)
+    return fail(SPC_ENOMEM, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  c->dev_allocs.push_back(*p);
+  c->dev_bytes += bytes;
+  return SPC_OK;
+}
+
+__nv_bfloat16* host_slab(spc_cache* c, __nv_bfloat16* base, int layer) {
+  return base + (size_t)(layer % c->G.host_layers) * c->slab_elems;
+}
+
+int check_layer(const spc_cache* c, int layer) {
+  if (!c) return fail(SPC_EINVAL, "null cache");
+  if (layer < 0 || layer >= c->G.layers) return fail(SPC_EINVAL, "layer out of range");
+  return SPC_OK;
+}
+
+void choose_splits(const spc_cache* c, int f, int* nsplit, int* bps) {
+  const Geo& G = c->G;
+  int nblk = f / G.g;
+  if (nblk <= 0) {
+    *nsplit = 1;
+    *bps = 1;
+    return;
+  }
+  int want = (2 * kNumSMs + G.H * G.batch - 1) / (G.H * G.batch);
+  want = std::max(1, std::min(want, std::min(kSplitCap, nblk)));
+  *bps = (nblk + want - 1) / want;
+  *nsplit = (nblk + *bps - 1) / *bps;
+}
+
+int migrate(spc_cache* c, int layer, cudaStream_t st) {
+  const Geo& G = c->G;
+  QuantSrc S{c->L[layer].ring_k, c->L[layer].ring_v, (long long)G.H * G.ring * G.d, (long long)G.d,
+             (long long)G.ring * G.d, G.ring};
+  // ring layout is [b][H][ring][d]: row stride d, head stride ring*d
+  launch_quantize(G, c->L[layer], S, (int)(c->f[layer] / G.g), 1, st);
+  CUDA_TRY(cudaGetLastError());
+  c->f[layer] += G.g;
+  return SPC_OK;
+}
+
+int append_rows(spc_cache* c, int layer, const void* kr, const void* vr, int64_t seq_stride,
+                cudaStream_t st) {
+  const Geo& G = c->G;
+  if (c->n[layer] >= c->context_length)
+    return fail(SPC_EINVAL, "context_length exceeded");
+  launch_append(G, c->L[layer], (const __nv_bfloat16*)kr, (const __nv_bfloat16*)vr,
+                seq_stride ? seq_stride : (int64_t)G.H * G.d, (int)c->n[layer],
+                host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer), st);
+  CUDA_TRY(cudaGetLastError());
+  c->n[layer] += 1;
+  while (c->n[layer] - c->f[layer] >= G.r + G.g) {  // kvcache.py:169-171
+    int rc = migrate(c, layer, st);
+    if (rc) return rc;
+  }
+  return SPC_OK;
+}
+
+int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_new,
+              const void* v_new, void* out, float* pinned_mass, cudaStream_t st) {
+  const Geo& G = c->G;
+  AttnArgs a{};
+  a.G = G;
+  a.B = c->L[layer];
+  a.q = (const __nv_bfloat16*)q;
+  a.k_new = (const __nv_bfloat16*)k_new;
+  a.v_new = (const __nv_bfloat16*)v_new;
+  a.out = (__nv_bfloat16*)out;
+  a.pinned_mass = pinned_mass;
+  a.rows = rows;
+  a.agg_row = rows - 1;  // decode: speculative row 1; predecode: row 0 (engine.py:262,317)
+  a.n = (int)c->n[layer];
+  a.f = (int)c->f[layer];
+  a.part_o = c->part_o;
+  a.part_ml = c->part_ml;
+  a.pin_ml = c->pin_ml;
+  a.spill = c->spill;
+  a.mz = c->mz;
+  a.sm_scale_log2 = (float)(1.0 / std::sqrt((double)G.d) * 1.4426950408889634);
+  bool fast = (c->impl != 1) && attend_fast_supported(G, rows);
+  if (c->impl == 2 && !fast) return fail(SPC_EINVAL, "fast attention path not available for this geometry");
+  if (fast) {
+    launch_attend_fast(a, st);  // chooses its own split plan
+  } else {
+    choose_splits(c, a.f, &a.nsplit, &a.blocks_per_split);
+    launch_attend_generic(a, st);
+    CUDA_TRY(cudaGetLastError());
+    launch_combine(a, st);
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaGetLastError());
+  launch_agg(a, st);
+  CUDA_TRY(cudaGetLastError());
+  // ticket: selection + prefetch on the copy stream (transfer.py:84-94)
+  CUDA_TRY(cudaEventRecord(c->ev_agg[layer], st));
+  CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev_agg[layer], 0));
+  launch_topk(G, c->L[layer], a.f, c->copy_stream);
+  CUDA_TRY(cudaGetLastError());
+  launch_prefetch(G, c->L[layer], host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer),
+                  c->copy_stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(c->ev_pf[layer], c->copy_stream));
+  return SPC_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int spc_abi_version(void) { return SPC_ABI_VERSION; }
+const char* spc_last_error(void) { return g_err.c_str(); }
+
+int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
+  if (!d || !out) return fail(SPC_EINVAL, "null argument");
+  *out = nullptr;
+  if (d->layers <= 0 || d->kv_heads <= 0 || d->head_dim <= 0)
+    return fail(SPC_EINVAL, "layers, kv_heads and head_dim must be positive");
+  if (!(d->bits == 1 || d->bits == 2 || d->bits == 4 || d->bits == 16))
+    return fail(SPC_EINVAL, "bits must be one of (1, 2, 4, 16)");
+  if (d->group_size <= 0 || d->residual <= 0 || d->prefetch_k <= 0 || d->context_length <= 0)
+    return fail(SPC_EINVAL, "group_size, residual, prefetch_k and context_length must be positive");
+  if (d->batch <= 0 || d->q_heads <= 0 || d->q_heads % d->kv_heads)
+    return fail(SPC_EINVAL, "q_heads must be a positive multiple of kv_heads and batch positive");
+  if (d->head_dim % 2 || d->head_dim > 256) return fail(SPC_EINVAL, "head_dim must be even and <= 256");
+  if (d->prefetch_k > 1024) return fail(SPC_EINVAL, "prefetch_k > 1024 unsupported");
+  if (2 * (d->q_heads / d->kv_heads) > 16) return fail(SPC_EINVAL, "more than 8 q heads per kv head unsupported");
+  if (d->group_size * d->head_dim > 12288) return fail(SPC_EINVAL, "group_size*head_dim too large");
+  if (d->topk_scope != SPC_SCOPE_LAYER && d->topk_scope != SPC_SCOPE_KV_HEAD)
+    return fail(SPC_EINVAL, "topk_scope must be 0 (layer) or 1 (kv_head)");
+  CUDA_TRY(cudaSetDevice(device));
+
+  spc_cache* c = new spc_cache();
+  c->device = device;
+  Geo& G = c->G;
+  G.layers = d->layers;
+  G.batch = d->batch;
+  G.H = d->kv_heads;
+  G.Hq = d->q_heads;
+  G.d = d->head_dim;
+  G.bits = d->bits;
+  G.g = d->group_size;
+  G.r = d->residual;
+  G.k = d->prefetch_k;
+  G.scope = d->topk_scope;
+  G.host_layers = (d->host_layers > 0 && d->host_layers <= d->layers) ? d->host_layers : d->layers;
+  G.G = G.Hq / G.H;
+  G.U = G.scope ? G.H : 1;
+  G.Hu = G.scope ? 1 : G.H;
+  c->context_length = d->context_length;
+  // capacity: whole blocks and whole bitmap words
+  int lcm = G.g;
+  while (lcm % 32) lcm += G.g;
+  G.L = (int)align_up((size_t)d->context_length, (size_t)lcm);
+  G.nblk = G.L / G.g;
+  G.ring = G.r + G.g;
+  G.nch = (G.d + G.g - 1) / G.g;
+  G.krw = G.bits == 16 ? G.d / 2 : (G.d * G.bits + 31) / 32;
+  G.vrw = G.krw;
+  G.fast = (G.d == 128 && G.g == 32 && (G.bits == 1 || G.bits == 2)) ? 1 : 0;
+  G.bwords = G.g * G.krw;
+
+  int rc = SPC_OK;
+  const size_t b = G.batch, H = G.H, U = G.U;
+  c->L.resize(G.layers);
+  for (int l = 0; l < G.layers && rc == SPC_OK; ++l) {
+    LayerBufs& B = c->L[l];
+    size_t codes = b * H * G.nblk * (size_t)G.bwords * 4;
+    size_t kpar = G.bits == 16 ? 0 : b * H * G.nblk * (size_t)G.d * 4;
+    size_t vpar = G.bits == 16 ? 0 : b * H * G.nblk * (size_t)G.g * G.nch * 4;
+    size_t ring = b * H * G.ring * (size_t)G.d * 2;
+    size_t pool = b * U * G.k * (size_t)G.Hu * G.d * 2;
+    size_t off[16], tot = 0, sizes[15] = {codes, codes, kpar, vpar, ring, ring, pool, pool,
+                                          b * U * G.k * 4, b * U * (G.L / 32) * 4, b * U * (size_t)G.L * 4,
+                                          b * U * G.k * 4, b * U * 4, b * U * G.k * 4, b * U * G.k * 4};
+    for (int i = 0; i < 15; ++i) {
+      off[i] = tot;
+      tot += align_up(std::max<size_t>(sizes[i], 16), 256);
+    }
+    char* base = nullptr;
+    rc = dalloc(c, (void**)&base, tot);
+    if (rc) break;
+    B.kcodes = (uint32_t*)(base + off[0]);
+    B.vcodes = (uint32_t*)(base + off[1]);
+    B.kparams = (uint32_t*)(base + off[2]);
+    B.vparams = (uint32_t*)(base + off[3]);
+    B.ring_k = (__nv_bfloat16*)(base + off[4]);
+    B.ring_v = (__nv_bfloat16*)(base + off[5]);
+    B.pool_k = (__nv_bfloat16*)(base + off[6]);
+    B.pool_v = (__nv_bfloat16*)(base + off[7]);
+    B.pin_pos = (int32_t*)(base + off[8]);
+    B.bitmap = (uint32_t*)(base + off[9]);
+    B.agg = (float*)(base + off[10]);
+    B.sel = (int32_t*)(base + off[11]);
+    B.newcnt = (int32_t*)(base + off[12]);
+    B.fetch_slot = (int32_t*)(base + off[13]);
+    B.fetch_pos = (int32_t*)(base + off[14]);
+    if (cudaMemset(B.pin_pos, 0xFF, sizes[8]) != cudaSuccess || cudaMemset(B.bitmap, 0, sizes[9]) != cudaSuccess ||
+        cudaMemset(B.sel, 0xFF, sizes[11]) != cudaSuccess || cudaMemset(B.newcnt, 0, sizes[12]) != cudaSuccess ||
+        cudaMemset(B.ring_k, 0, ring) != cudaSuccess || cudaMemset(B.ring_v, 0, ring) != cudaSuccess ||
+        cudaMemset(B.pool_k, 0, pool) != cudaSuccess || cudaMemset(B.pool_v, 0, pool) != cudaSuccess)
+      rc = fail(SPC_ECUDA, "cudaMemset failed");
+  }
+  const size_t R = 2 * G.G;
+  if (rc == SPC_OK) rc = dalloc(c, (void**)&c->part_o, b * H * (kSplitCap + 1) * R * G.d * 4);
+  if (rc == SPC_OK) rc = dalloc(c, (void**)&c->part_ml, b * H * (kSplitCap + 1) * R * 2 * 4);
+  if (rc == SPC_OK) rc = dalloc(c, (void**)&c->pin_ml, b * H * R * 2 * 4);
+  if (rc == SPC_OK) rc = dalloc(c, (void**)&c->spill, b * G.Hq * (size_t)G.L * 4);
+  if (rc == SPC_OK) rc = dalloc(c, (void**)&c->mz, b * G.Hq * 2 * 4);
+  if (rc == SPC_OK) rc = dalloc(c, (void**)&c->staging, (size_t)G.k * 4);
+  if (rc == SPC_OK) {
+    c->slab_elems = b * (size_t)G.L * H * G.d;
+    c->host_bytes = 2 * c->slab_elems * G.host_layers * sizeof(__nv_bfloat16);
+    cudaError_t e1 = cudaHostAlloc((void**)&c->host_k, c->host_bytes / 2, cudaHostAllocMapped | cudaHostAllocPortable);
+    cudaError_t e2 = e1 == cudaSuccess ? cudaHostAlloc((void**)&c->host_v, c->host_bytes / 2,
+                                                       cudaHostAllocMapped | cudaHostAllocPortable)
+                                       : e1;
+    if (e1 != cudaSuccess || e2 != cudaSuccess)
+      rc = fail(SPC_ENOMEM, std::string("pinned host slow tier (") + std::to_string(c->host_bytes) +
+                                " bytes): " + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  }
+  if (rc == SPC_OK) {
+    if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+      rc = fail(SPC_ECUDA, "stream create failed");
+    c->ev_agg.resize(G.layers);
+    c->ev_pf.resize(G.layers);
+    for (int l = 0; l < G.layers && rc == SPC_OK; ++l) {
+      if (cudaEventCreateWithFlags(&c->ev_agg[l], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c->ev_pf[l], cudaEventDisableTiming) != cudaSuccess)
+        rc = fail(SPC_ECUDA, "event create failed");
+    }
+  }
+  if (rc == SPC_OK && cudaDeviceSynchronize() != cudaSuccess) rc = fail(SPC_ECUDA, "init sync failed");
+  c->n.assign(G.layers, 0);
+  c->f.assign(G.layers, 0);
+  c->ticket.assign(G.layers, -1);
+  if (rc != SPC_OK) {
+    std::string keep = g_err;
+    spc_cache_destroy(c);
+    g_err = keep;
+    return rc;
+  }
+  *out = c;
+  return SPC_OK;
+}
+
+int spc_cache_destroy(spc_cache* c) {
+  if (!c) return SPC_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (void* p : c->dev_allocs) cudaFree(p);
+  if (c->host_k) cudaFreeHost(c->host_k);
+  if (c->host_v) cudaFreeHost(c->host_v);
+  for (auto e : c->ev_agg) if (e) cudaEventDestroy(e);
+  for (auto e : c->ev_pf) if (e) cudaEventDestroy(e);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  delete c;
+  return SPC_OK;
+}
+
+int spc_cache_fast_path(const spc_cache* c) { return c && c->G.fast ? attend_fast_supported(c->G, 2) : 0; }
+int64_t spc_device_bytes(const spc_cache* c) { return c ? (int64_t)c->dev_bytes : -1; }
+int64_t spc_host_bytes(const spc_cache* c) { return c ? (int64_t)c->host_bytes : -1; }
+int64_t spc_length(const spc_cache* c, int layer) { return check_layer(c, layer) ? -1 : c->n[layer]; }
+int64_t spc_frontier(const spc_cache* c, int layer) { return check_layer(c, layer) ? -1 : c->f[layer]; }
+int64_t spc_row_bytes(const spc_cache* c, int64_t positions) {
+  // kvcache.py:148-150: 16-bit accounting, key + value rows, all kv heads
+  return c ? positions * 2 * c->G.d * 2 * c->G.H : -1;
+}
+
+int spc_set_attend_impl(spc_cache* c, int impl) {
+  if (!c || impl < 0 || impl > 2) return fail(SPC_EINVAL, "impl must be 0 (auto), 1 (generic) or 2 (fast)");
+  c->impl = impl;
+  return SPC_OK;
+}
+
+int spc_prefill(spc_cache* c, int layer, const void* K, const void* V, int n, void* stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  const Geo& G = c->G;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (c->n[layer] != 0) return fail(SPC_EPROTO, "prefill requires an empty layer");
+  if (n <= 0) return fail(SPC_EINVAL, "prompt must be nonempty");
+  if (n > c->context_length) return fail(SPC_EINVAL, "prompt longer than context_length");
+  CUDA_TRY(cudaSetDevice(c->device));
+  // slow tier: every row (kvcache.py:165-166)
+  size_t row = (size_t)G.H * G.d * sizeof(__nv_bfloat16);
+  CUDA_TRY(cudaMemcpy2DAsync(host_slab(c, c->host_k, layer), (size_t)G.L * row, K, (size_t)n * row,
+                             (size_t)n * row, G.batch, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpy2DAsync(host_slab(c, c->host_v, layer), (size_t)G.L * row, V, (size_t)n * row,
+                             (size_t)n * row, G.batch, cudaMemcpyDeviceToHost, st));
+  int64_t f = frontier_of(n, G.r, G.g);
+  QuantSrc S{(const __nv_bfloat16*)K, (const __nv_bfloat16*)V, (long long)n * G.H * G.d,
+             (long long)G.H * G.d, (long long)G.d, 0};
+  launch_quantize(G, c->L[layer], S, 0, (int)(f / G.g), st);
+  CUDA_TRY(cudaGetLastError());
+  launch_ring_fill(G, c->L[layer], (const __nv_bfloat16*)K, (const __nv_bfloat16*)V, n, (int)f, st);
+  CUDA_TRY(cudaGetLastError());
+  c->n[layer] = n;
+  c->f[layer] = f;
+  return SPC_OK;
+}
+
+int spc_append(spc_cache* c, int layer, const void* k_rows, const void* v_rows, int64_t seq_stride,
+               void* stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  CUDA_TRY(cudaSetDevice(c->device));
+  return append_rows(c, layer, k_rows, v_rows, seq_stride, (cudaStream_t)stream);
+}
+
+int spc_migrate(spc_cache* c, int layer, void* stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  if (c->n[layer] - c->f[layer] < c->G.g)  // kvcache.py:175-177
+    return fail(SPC_EINVAL, "not enough residual tokens to migrate");
+  CUDA_TRY(cudaSetDevice(c->device));
+  return migrate(c, layer, (cudaStream_t)stream);
+}
+
+int spc_select_topk(const float* scores, int n, int k, int32_t* out, void* stream) {
+  if (n < 0 || k < 0 || k > 1024) return fail(SPC_EINVAL, "select_topk: need n >= 0 and 0 <= k <= 1024");
+  if (k == 0) return SPC_OK;
+  launch_select(scores, n, k, out, (cudaStream_t)stream);
+  CUDA_TRY(cudaGetLastError());
+  return SPC_OK;
+}
+
+int spc_pin(spc_cache* c, int layer, int seq, int unit, const int32_t* positions, int npos,
+            const void* k_rows, const void* v_rows, void* stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  const Geo& G = c->G;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (seq < 0 || seq >= G.batch || unit < 0 || unit >= G.U) return fail(SPC_EINVAL, "seq/unit out of range");
+  if (npos > G.k) return fail(SPC_EINVAL, "pinned set larger than the prefetch budget");
+  std::vector<int32_t> p(positions, positions + std::max(npos, 0));
+  for (int32_t x : p) {  // kvcache.py:202-209
+    if (x < 0 || x >= c->n[layer]) return fail(SPC_EINVAL, "position " + std::to_string(x) + " does not exist");
+    if (x >= c->f[layer]) return fail(SPC_EINVAL, "position " + std::to_string(x) + " is inside the residual window");
+  }
+  std::sort(p.begin(), p.end());
+  p.erase(std::unique(p.begin(), p.end()), p.end());
+  if (k_rows && (int)p.size() != npos) return fail(SPC_EINVAL, "duplicate positions with explicit rows");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));  // no selection in flight
+  if (!p.empty())
+    CUDA_TRY(cudaMemcpyAsync(c->staging, p.data(), p.size() * 4, cudaMemcpyHostToDevice, st));
+  launch_set_pins(G, c->L[layer], seq, unit, c->staging, (int)p.size(), st);
+  if (k_rows && v_rows) {
+    launch_copy_pins(G, c->L[layer], seq, unit, (const __nv_bfloat16*)k_rows, (const __nv_bfloat16*)v_rows,
+                     (int)p.size(), st);
+  } else {
+    // slow-tier fetch of every pinned row (pin() default, kvcache.py:208-209)
+    launch_prefetch_one(G, c->L[layer], seq, unit, host_slab(c, c->host_k, layer),
+                        host_slab(c, c->host_v, layer), st);
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));  // staging buffer reuse + host vector lifetime
+  return SPC_OK;
+}
+
+int spc_predecode_layer(spc_cache* c, int layer, const void* q, const void* k_new, const void* v_new,
+                        void* out, void* stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  if (c->ticket[layer] != -1)
+    return fail(SPC_EPROTO, "duplicate ticket for step 0 layer " + std::to_string(layer));
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));
+  int rc = run_layer(c, layer, 1, q, k_new, v_new, out, nullptr, st);
+  if (rc) return rc;
+  c->ticket[layer] = 0;
+  return SPC_OK;
+}
+
+int spc_decode_layer(spc_cache* c, int layer, int step, const void* q, const void* k_new,
+                     const void* v_new, void* out, float* pinned_mass, void* stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  if (c->ticket[layer] != step - 1)  // transfer.py:96-100
+    return fail(SPC_EPROTO, "no ticket was issued at step " + std::to_string(step - 1) + " for layer " +
+                                std::to_string(layer));
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));  // await_layer
+  c->ticket[layer] = -1;
+  int rc = run_layer(c, layer, 2, q, k_new, v_new, out, pinned_mass, st);
+  if (rc) return rc;
+  c->ticket[layer] = step;
+  // persist row 0 only (engine.py:321; SPEC: the speculative row is never persisted)
+  return append_rows(c, layer, k_new, v_new, (int64_t)2 * c->G.H * c->G.d, st);
+}
+
+int spc_ticket(spc_cache* c, int layer, int32_t* picked, int32_t* new_count, void* stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  const Geo& G = c->G;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));
+  if (picked)
+    CUDA_TRY(cudaMemcpyAsync(picked, c->L[layer].sel, (size_t)G.batch * G.U * G.k * 4, cudaMemcpyDeviceToDevice, st));
+  if (new_count)
+    CUDA_TRY(cudaMemcpyAsync(new_count, c->L[layer].newcnt, (size_t)G.batch * G.U * 4, cudaMemcpyDeviceToDevice, st));
+  return SPC_OK;
+}
+
+int spc_debug_agg(spc_cache* c, int layer, float* agg, void* stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  const Geo& G = c->G;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));
+  CUDA_TRY(cudaMemcpyAsync(agg, c->L[layer].agg, (size_t)G.batch * G.U * G.L * 4, cudaMemcpyDeviceToDevice, st));
+  return SPC_OK;
+}
+
+int spc_materialize(spc_cache* c, int layer, int seq, int head, float* keys, float* values, void* stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  if (seq < 0 || seq >= c->G.batch || head < 0 || head >= c->G.H) return fail(SPC_EINVAL, "seq/head out of range");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));
+  launch_materialize(c->G, c->L[layer], seq, head, (int)c->n[layer], (int)c->f[layer], keys, values, st);
+  CUDA_TRY(cudaGetLastError());
+  return SPC_OK;
+}
+
+int spc_export_packed(spc_cache* c, int layer, int seq, uint8_t* kc, uint16_t* kz, uint16_t* ks,
+                      uint8_t* vc, uint16_t* vz, uint16_t* vs, void* stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  if (c->G.bits == 16) return fail(SPC_EINVAL, "16-bit tier has no packed groups");
+  if (seq < 0 || seq >= c->G.batch) return fail(SPC_EINVAL, "seq out of range");
+  launch_export(c->G, c->L[layer], seq, (int)(c->f[layer] / c->G.g), kc, kz, ks, vc, vz, vs,
+                (cudaStream_t)stream);
+  CUDA_TRY(cudaGetLastError());
+  return SPC_OK;
+}
+
+int spc_slow_fetch(spc_cache* c, int layer, int seq, const int32_t* positions, int npos, void* k_out,
+                   void* v_out) {
+  if (int rc = check_layer(c, layer)) return rc;
+  const Geo& G = c->G;
+  if (seq < 0 || seq >= G.batch) return fail(SPC_EINVAL, "seq out of range");
+  for (int i = 0; i < npos; ++i)  // kvcache.py:250-252
+    if (positions[i] < 0 || positions[i] >= c->n[layer])
+      return fail(SPC_EINVAL, "position " + std::to_string(positions[i]) + " not present in the slow tier");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  const size_t row = (size_t)G.H * G.d;
+  const __nv_bfloat16* hk = host_slab(c, c->host_k, layer) + (size_t)seq * G.L * row;
+  const __nv_bfloat16* hv = host_slab(c, c->host_v, layer) + (size_t)seq * G.L * row;
+  for (int i = 0; i < npos; ++i) {
+    std::memcpy((char*)k_out + i * row * 2, hk + (size_t)positions[i] * row, row * 2);
+    std::memcpy((char*)v_out + i * row * 2, hv + (size_t)positions[i] * row, row * 2);
+  }
+  return SPC_OK;
+}
+
+int spc_pin_state(spc_cache* c, int layer, const int32_t** pin_pos) {
+  if (int rc = check_layer(c, layer)) return rc;
+  *pin_pos = c->L[layer].pin_pos;
+  return SPC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,348 @@
+// select.cu -- K4 top-k selection + pin diff, K5 prefetch gather, K6 append.
+//
+// K4 replaces select_topk (engine.py:75-84) + the pin-set diff of
+// _issue_ticket (engine.py:270-284) + pin (kvcache.py:194-218): a radix select
+// over the fp32 bit patterns of agg (agg >= 0, so uint32 order == float order),
+// ties to the lower position, emitted ascending; retained pins keep their slot,
+// new pins take the slots of dropped pins, and only new pins are fetched
+// (bytes charged = row_bytes(|new|), engine.py:274-276).
+//
+// K5 replaces slow_fetch + the ticket's worker fetch (kvcache.py:245-259,
+// transfer.py:126-144): a zero-copy gather of the new rows from the pinned
+// host slow tier over PCIe into the device slot pool, on the copy stream.
+//
+// K6 replaces append_verified (kvcache.py:162-171): row 0's K/V go to the
+// residual ring (HBM) and to the slow tier (pinned host, zero-copy store).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace spc {
+
+namespace {
+constexpr int kTopkThreads = 1024;
+constexpr int kMaxK = 1024;
+
+__device__ inline int block_exclusive_scan(int v, int* warp_sums, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) warp_sums[lane] = w;  // inclusive
+    if (lane == nw - 1) *total = w;
+  }
+  __syncthreads();
+  int before = (warp ? warp_sums[warp - 1] : 0) + x - v;
+  __syncthreads();
+  return before;
+}
+}  // namespace
+
+// Radix select of the K largest of agg[0, f) (uint32 bit patterns of
+// non-negative fp32), ties to the lower position, written ascending to sel[].
+// Whole-CTA cooperative (kTopkThreads threads).
+__device__ void select_topk_cta(const uint32_t* __restrict__ agg, int f, int K, int* sel) {
+  const int tid = threadIdx.x;
+  __shared__ int hist[256];
+  __shared__ int warp_sums[32];
+  __shared__ int s_total, s_digit, s_remaining;
+  uint32_t prefix = 0, pmask = 0;
+  int remaining = K;
+  if (K > 0) {
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = tid; i < 256; i += kTopkThreads) hist[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < f; i += kTopkThreads) {
+        uint32_t v = agg[i];
+        if ((v & pmask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1);
+      }
+      __syncthreads();
+      if (tid < 32) {
+        // find the digit, scanning bins from the top (warp-cooperative)
+        int acc = 0, found = -1, before = 0;
+        for (int base = 224; base >= 0 && found < 0; base -= 32) {
+          int bin = base + (31 - tid);  // lane 0 -> highest bin of this slab
+          int c = hist[bin];
+          int x = c;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (tid >= o) x += y;
+          }
+          // x = count in bins [bin, base+31] (inclusive prefix from the top)
+          unsigned hit = __ballot_sync(0xffffffffu, acc + x >= remaining);
+          if (hit) {
+            int l = __ffs(hit) - 1;
+            int xl = __shfl_sync(0xffffffffu, x, l), cl = __shfl_sync(0xffffffffu, c, l);
+            found = base + 31 - l;
+            before = acc + xl - cl;
+          } else {
+            acc += __shfl_sync(0xffffffffu, x, 31);
+          }
+        }
+        if (tid == 0) {
+          s_digit = found;
+          s_remaining = remaining - before;
+        }
+      }
+      __syncthreads();
+      prefix |= (uint32_t)s_digit << shift;
+      pmask |= 255u << shift;
+      remaining = s_remaining;
+      __syncthreads();
+    }
+  }
+  const uint32_t T = prefix;
+  const int need_eq = remaining;  // elements == T to take, lowest positions first
+  // selection in position order: thread owns a contiguous range
+  const int per = (f + kTopkThreads - 1) / kTopkThreads;
+  const int i0 = min(f, tid * per), i1 = min(f, i0 + per);
+  int n_gt = 0, n_eq = 0;
+  if (K > 0)
+    for (int i = i0; i < i1; ++i) {
+      uint32_t v = agg[i];
+      n_gt += v > T;
+      n_eq += v == T;
+    }
+  int eq_before = block_exclusive_scan(n_eq, warp_sums, &s_total);
+  int take_eq = max(0, min(n_eq, need_eq - eq_before));
+  int my_sel = (K > 0) ? n_gt + take_eq : 0;
+  int out = block_exclusive_scan(my_sel, warp_sums, &s_total);
+  if (my_sel) {
+    int eq_seen = 0;
+    for (int i = i0; i < i1; ++i) {
+      uint32_t v = agg[i];
+      bool take = v > T || (v == T && eq_seen++ < take_eq);
+      if (take) sel[out++] = i;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kTopkThreads) k_topk(Geo G, LayerBufs B, int f) {
+  const int u = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const size_t bu = (size_t)b * G.U + u;
+  const uint32_t* agg = reinterpret_cast<const uint32_t*>(B.agg + bu * G.L);
+  const int K = min(G.k, f);
+  __shared__ int warp_sums[32];
+  __shared__ int s_total;
+  __shared__ int sel[kMaxK];
+  __shared__ int keep[kMaxK];
+  __shared__ int freelist[kMaxK];
+  __shared__ int newlist[kMaxK];
+  select_topk_cta(agg, f, K, sel);
+  // ---- pin diff + slot assignment ------------------------------------------------
+  int32_t* pin_pos = B.pin_pos + bu * G.k;
+  uint32_t* bitmap = B.bitmap + bu * (G.L / 32);
+  for (int s = tid; s < G.k; s += kTopkThreads) {
+    int p = pin_pos[s], kp = 0;
+    if (p >= 0) {  // binary search in the ascending selection
+      int lo = 0, hi = K - 1;
+      while (lo <= hi) {
+        int mid = (lo + hi) >> 1;
+        int v = sel[mid];
+        if (v == p) { kp = 1; break; }
+        if (v < p) lo = mid + 1; else hi = mid - 1;
+      }
+    }
+    keep[s] = kp;
+  }
+  int is_new_cnt = 0, my_new[8];  // K <= kMaxK = 1024 -> at most 1 per thread
+  for (int i = tid; i < K; i += kTopkThreads) {
+    int p = sel[i];
+    bool pinned = (bitmap[p >> 5] >> (p & 31)) & 1u;
+    if (!pinned) my_new[is_new_cnt++] = p;
+  }
+  __syncthreads();
+  int nfree_mine = 0;
+  for (int s = tid; s < G.k; s += kTopkThreads) nfree_mine += !keep[s];
+  int free_off = block_exclusive_scan(nfree_mine, warp_sums, &s_total);
+  for (int s = tid; s < G.k; s += kTopkThreads)
+    if (!keep[s]) freelist[free_off++] = s;
+  int new_off = block_exclusive_scan(is_new_cnt, warp_sums, &s_total);
+  const int nnew = s_total;
+  for (int x = 0; x < is_new_cnt; ++x) newlist[new_off + x] = my_new[x];
+  __syncthreads();
+  // drop pins that were not re-selected
+  for (int s = tid; s < G.k; s += kTopkThreads) {
+    int p = pin_pos[s];
+    if (p >= 0 && !keep[s]) {
+      atomicAnd(&bitmap[p >> 5], ~(1u << (p & 31)));
+      pin_pos[s] = -1;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < nnew; i += kTopkThreads) {
+    int slot = freelist[i], p = newlist[i];
+    pin_pos[slot] = p;
+    atomicOr(&bitmap[p >> 5], 1u << (p & 31));
+    B.fetch_slot[bu * G.k + i] = slot;
+    B.fetch_pos[bu * G.k + i] = p;
+  }
+  for (int i = tid; i < G.k; i += kTopkThreads) B.sel[bu * G.k + i] = i < K ? sel[i] : -1;
+  if (tid == 0) B.newcnt[bu] = nnew;
+}
+
+void launch_topk(const Geo& G, const LayerBufs& B, int f, cudaStream_t st) {
+  k_topk<<<dim3(G.U, G.batch), kTopkThreads, 0, st>>>(G, B, f);
+}
+
+// Standalone select_topk (engine.py:75-84) over eligible = [0, n): out[k]
+// ascending, -1 padded.  Used by the K4 parity tests on exact inputs.
+__global__ void __launch_bounds__(kTopkThreads) k_select(const float* scores, int n, int k, int32_t* out) {
+  __shared__ int sel[kMaxK];
+  const int K = min(k, n);
+  select_topk_cta(reinterpret_cast<const uint32_t*>(scores), n, K, sel);
+  for (int i = threadIdx.x; i < k; i += kTopkThreads) out[i] = i < K ? sel[i] : -1;
+}
+
+void launch_select(const float* scores, int n, int k, int32_t* out, cudaStream_t st) {
+  k_select<<<1, kTopkThreads, 0, st>>>(scores, n, k, out);
+}
+
+// Explicit pin() from the host API: replace the pinned set of one (seq, unit)
+// with `pos` (ascending, unique, validated on the host), slot i <- pos[i].
+__global__ void k_set_pins(Geo G, LayerBufs B, int seq, int unit, const int32_t* pos, int npos) {
+  const size_t bu = (size_t)seq * G.U + unit;
+  int32_t* pin_pos = B.pin_pos + bu * G.k;
+  uint32_t* bitmap = B.bitmap + bu * (G.L / 32);
+  for (int s = threadIdx.x; s < G.k; s += blockDim.x) {
+    int p = pin_pos[s];
+    if (p >= 0) atomicAnd(&bitmap[p >> 5], ~(1u << (p & 31)));
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < G.k; s += blockDim.x) {
+    int p = s < npos ? pos[s] : -1;
+    pin_pos[s] = p;
+    if (p >= 0) {
+      atomicOr(&bitmap[p >> 5], 1u << (p & 31));
+      B.fetch_slot[bu * G.k + s] = s;
+      B.fetch_pos[bu * G.k + s] = p;
+    }
+    B.sel[bu * G.k + s] = p;
+  }
+  if (threadIdx.x == 0) B.newcnt[bu] = npos;
+}
+
+void launch_set_pins(const Geo& G, const LayerBufs& B, int seq, int unit, const int32_t* pos,
+                     int npos, cudaStream_t st) {
+  k_set_pins<<<1, 256, 0, st>>>(G, B, seq, unit, pos, npos);
+}
+
+// K5: one CTA per (new-pin index, unit, seq).  Rows of a unit's heads are
+// contiguous in the host tier ([pos][H][d]), so a layer-scope pin moves one
+// contiguous H*d*2-byte K row and one V row with 16-byte zero-copy loads.
+__global__ void __launch_bounds__(256) k_prefetch(Geo G, LayerBufs B, const uint4* host_k,
+                                                  const uint4* host_v, int seq0, int unit0) {
+  const int i = blockIdx.x, u = blockIdx.y + unit0, b = blockIdx.z + seq0;
+  const size_t bu = (size_t)b * G.U + u;
+  if (i >= B.newcnt[bu]) return;
+  const int slot = B.fetch_slot[bu * G.k + i], pos = B.fetch_pos[bu * G.k + i];
+  const int h0 = G.scope ? u : 0;
+  if (G.d % 8) {  // small / odd head dims: element copies
+    const __nv_bfloat16* hk = reinterpret_cast<const __nv_bfloat16*>(host_k);
+    const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(host_v);
+    const size_t src = (((size_t)b * G.L + pos) * G.H + h0) * G.d;
+    const size_t dst = ((bu * G.k + slot) * G.Hu) * G.d;
+    for (int x = threadIdx.x; x < G.Hu * G.d; x += blockDim.x) {
+      B.pool_k[dst + x] = hk[src + x];
+      B.pool_v[dst + x] = hv[src + x];
+    }
+    return;
+  }
+  const int vec = G.Hu * G.d / 8;  // uint4 per row
+  const size_t src = (((size_t)b * G.L + pos) * G.H + h0) * G.d / 8;
+  const size_t dst = ((bu * G.k + slot) * G.Hu) * G.d / 8;
+  uint4* pk = reinterpret_cast<uint4*>(B.pool_k);
+  uint4* pv = reinterpret_cast<uint4*>(B.pool_v);
+  for (int x = threadIdx.x; x < vec; x += blockDim.x) {
+    uint4 a = host_k[src + x];
+    uint4 c = host_v[src + x];
+    pk[dst + x] = a;
+    pv[dst + x] = c;
+  }
+}
+
+void launch_prefetch(const Geo& G, const LayerBufs& B, const __nv_bfloat16* host_k,
+                     const __nv_bfloat16* host_v, cudaStream_t st) {
+  k_prefetch<<<dim3(G.k, G.U, G.batch), 256, 0, st>>>(
+      G, B, reinterpret_cast<const uint4*>(host_k), reinterpret_cast<const uint4*>(host_v), 0, 0);
+}
+
+void launch_prefetch_one(const Geo& G, const LayerBufs& B, int seq, int unit,
+                         const __nv_bfloat16* host_k, const __nv_bfloat16* host_v, cudaStream_t st) {
+  k_prefetch<<<dim3(G.k, 1, 1), 256, 0, st>>>(
+      G, B, reinterpret_cast<const uint4*>(host_k), reinterpret_cast<const uint4*>(host_v), seq, unit);
+}
+
+// pin() with caller-supplied rows: device bf16 [npos][Hu][d] -> slots 0..npos-1
+__global__ void k_copy_pins(Geo G, LayerBufs B, int seq, int unit, const __nv_bfloat16* kr,
+                            const __nv_bfloat16* vr) {
+  const int s = blockIdx.x;
+  const size_t dst = ((((size_t)seq * G.U + unit) * G.k + s) * G.Hu) * G.d;
+  const size_t src = (size_t)s * G.Hu * G.d;
+  for (int x = threadIdx.x; x < G.Hu * G.d; x += blockDim.x) {
+    B.pool_k[dst + x] = kr[src + x];
+    B.pool_v[dst + x] = vr[src + x];
+  }
+}
+
+void launch_copy_pins(const Geo& G, const LayerBufs& B, int seq, int unit, const __nv_bfloat16* k_rows,
+                      const __nv_bfloat16* v_rows, int npos, cudaStream_t st) {
+  if (npos > 0) k_copy_pins<<<npos, 256, 0, st>>>(G, B, seq, unit, k_rows, v_rows);
+}
+
+// K6: append row 0 at position n: residual ring slot n % (r+g) and slow tier.
+__global__ void k_append(Geo G, LayerBufs B, const __nv_bfloat16* kr, const __nv_bfloat16* vr,
+                         long long seq_stride, int n, __nv_bfloat16* host_k, __nv_bfloat16* host_v) {
+  const int b = blockIdx.x;
+  const int slot = n % G.ring;
+  for (int x = threadIdx.x; x < G.H * G.d; x += blockDim.x) {
+    int h = x / G.d, c = x - h * G.d;
+    __nv_bfloat16 kv = kr[(size_t)b * seq_stride + x], vv = vr[(size_t)b * seq_stride + x];
+    size_t ro = (((size_t)b * G.H + h) * G.ring + slot) * G.d + c;
+    B.ring_k[ro] = kv;
+    B.ring_v[ro] = vv;
+    size_t ho = (((size_t)b * G.L + n) * G.H + h) * G.d + c;
+    host_k[ho] = kv;
+    host_v[ho] = vv;
+  }
+}
+
+void launch_append(const Geo& G, const LayerBufs& B, const __nv_bfloat16* k_rows,
+                   const __nv_bfloat16* v_rows, long long seq_stride, int n,
+                   __nv_bfloat16* host_k, __nv_bfloat16* host_v, cudaStream_t st) {
+  k_append<<<G.batch, 256, 0, st>>>(G, B, k_rows, v_rows, seq_stride, n, host_k, host_v);
+}
+
+// Prefill: residual rows [f, n) of K/V [b][n][H][d] into the ring.
+__global__ void k_ring_fill(Geo G, LayerBufs B, const __nv_bfloat16* K, const __nv_bfloat16* V,
+                            int n, int f) {
+  const int pos = f + blockIdx.x, b = blockIdx.y;
+  const int slot = pos % G.ring;
+  for (int x = threadIdx.x; x < G.H * G.d; x += blockDim.x) {
+    int h = x / G.d, c = x - h * G.d;
+    size_t src = (((size_t)b * n + pos) * G.H + h) * G.d + c;
+    size_t ro = (((size_t)b * G.H + h) * G.ring + slot) * G.d + c;
+    B.ring_k[ro] = K[src];
+    B.ring_v[ro] = V[src];
+  }
+}
+
+void launch_ring_fill(const Geo& G, const LayerBufs& B, const __nv_bfloat16* K,
+                      const __nv_bfloat16* V, int n, int f, cudaStream_t st) {
+  if (n > f) k_ring_fill<<<dim3(n - f, G.batch), 256, 0, st>>>(G, B, K, V, n, f);
+}
+
+}  // namespace spc

@@ -1,0 +1,141 @@
+"""The dual-token decode step of SpeCache, one layer at a time, on the device.
+
+Reference: SpeculativeDecoder.predecode (engine.py:245-268) and the per-layer
+body of SpeculativeDecoder.decode_step (engine.py:299-321), fed post-RoPE
+q/k/v.  The projections, FFN and logits around it are outside the hot path;
+callers hand in q [batch, rows, q_heads, d] and k_new/v_new
+[batch, rows, kv_heads, d] (rows = 1 predecode, 2 decode: row 0 verified at
+position n, row 1 speculative at n+1).
+
+Per call the library launches, on the caller's stream: K2 attention over the
+packed low-bit tier + pinned/residual/in-step rows, K3 combine + cross-head
+aggregate; on its copy stream K4 top-k + pin diff and K5 the PCIe prefetch of
+the new pins (the ticket); then K6 append of row 0.  The next decode_layer of
+the same layer waits on that ticket's event (await_layer).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .cache import DeviceTwoTierCache, current_stream, to_device_bf16
+
+__all__ = ["LayerResult", "StepMetrics", "SpeculativeLayerDecoder", "select_topk"]
+
+
+@dataclass
+class StepMetrics:
+    """engine.py:164-172."""
+    step: int
+    token: int
+    speculative_hit: bool
+    pinned_mass: float
+    bytes_fetched: int
+    new_pins: int
+    tokens_emitted: int = 1
+
+
+@dataclass
+class LayerResult:
+    out: "object"          # torch bf16 [batch, rows, q_heads, d]
+    pinned_mass: "object"  # torch fp32 [batch, q_heads] (decode only)
+
+
+class SpeculativeLayerDecoder:
+    """Drives one DeviceTwoTierCache through predecode / decode steps.
+
+    Phase rules follow the reference state machine (engine.py:221-222,
+    247-248, 288-289) per layer; ticket rules follow transfer.py:84-100 and are
+    enforced by the C library (ProtocolError)."""
+
+    def __init__(self, cache: DeviceTwoTierCache):
+        self.cache = cache
+        self._dev = cache._torch_device
+
+    def _inputs(self, q, k_new, v_new, rows):
+        c = self.cache
+        q = to_device_bf16(q, self._dev)
+        k = to_device_bf16(k_new, self._dev)
+        v = to_device_bf16(v_new, self._dev)
+        if q.dim() == 3:
+            q, k, v = q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0)
+        if tuple(q.shape) != (c.batch, rows, c.q_heads, c.head_dim):
+            raise ValueError(f"q must be [batch, {rows}, q_heads, head_dim]")
+        if tuple(k.shape) != (c.batch, rows, c.kv_heads, c.head_dim) or k.shape != v.shape:
+            raise ValueError(f"k_new/v_new must be [batch, {rows}, kv_heads, head_dim]")
+        return q, k, v
+
+    def predecode_layer(self, layer: int, q, k_new, v_new, out=None):
+        import torch
+        c = self.cache
+        q, k, v = self._inputs(q, k_new, v_new, 1)
+        if out is None:
+            out = torch.empty_like(q)
+        _lib.check(_lib.lib().spc_predecode_layer(c.handle, layer, q.data_ptr(), k.data_ptr(),
+                                                  v.data_ptr(), out.data_ptr(),
+                                                  current_stream(self._dev)))
+        self._keep = (q, k, v)
+        return out
+
+    def decode_layer(self, layer: int, step: int, q, k_new, v_new, out=None,
+                     pinned_mass=None) -> LayerResult:
+        import torch
+        c = self.cache
+        q, k, v = self._inputs(q, k_new, v_new, 2)
+        if out is None:
+            out = torch.empty_like(q)
+        if pinned_mass is None:
+            pinned_mass = torch.empty((c.batch, c.q_heads), dtype=torch.float32, device=self._dev)
+        _lib.check(_lib.lib().spc_decode_layer(c.handle, layer, step, q.data_ptr(), k.data_ptr(),
+                                               v.data_ptr(), out.data_ptr(), pinned_mass.data_ptr(),
+                                               current_stream(self._dev)))
+        self._keep = (q, k, v)
+        return LayerResult(out, pinned_mass)
+
+    def ticket(self, layer: int):
+        """(picked int32 [batch, units, k] ascending -1 padded, new_count int32 [batch, units])
+        of the last ticket issued for ``layer``."""
+        import torch
+        c = self.cache
+        picked = torch.empty((c.batch, c.units, c.budget.prefetch_k), dtype=torch.int32, device=self._dev)
+        newc = torch.empty((c.batch, c.units), dtype=torch.int32, device=self._dev)
+        _lib.check(_lib.lib().spc_ticket(c.handle, layer, picked.data_ptr(), newc.data_ptr(),
+                                         current_stream(self._dev)))
+        return picked, newc
+
+    def debug_agg(self, layer: int):
+        import torch
+        c = self.cache
+        L = _capacity(c)
+        agg = torch.empty((c.batch, c.units, L), dtype=torch.float32, device=self._dev)
+        _lib.check(_lib.lib().spc_debug_agg(c.handle, layer, agg.data_ptr(), current_stream(self._dev)))
+        return agg
+
+
+def _capacity(c: DeviceTwoTierCache) -> int:
+    g = c.budget.group_size
+    lcm = g
+    while lcm % 32:
+        lcm += g
+    L = c.budget.context_length
+    return (L + lcm - 1) // lcm * lcm
+
+
+def select_topk(scores, k: int, eligible=None, device: int = 0) -> tuple:
+    """Device select_topk (engine.py:75-84) for eligible = range(n) (the
+    packed-positions domain): k highest, ties to the lower position, sorted."""
+    import torch
+    s = torch.as_tensor(np.asarray(scores, np.float32), device=f"cuda:{device}")
+    n = s.numel() if eligible is None else len(eligible)
+    if eligible is not None and list(eligible) != list(range(n)):
+        raise ValueError("device select_topk supports eligible = range(n)")
+    if k <= 0 or n == 0:
+        return ()
+    if bool((s[:n] < 0).any()):
+        raise ValueError("device select_topk expects non-negative scores (probability mass)")
+    out = torch.empty(k, dtype=torch.int32, device=s.device)
+    _lib.check(_lib.lib().spc_select_topk(s.data_ptr(), n, k, out.data_ptr(),
+                                          current_stream(s.device)))
+    return tuple(int(p) for p in out.cpu().tolist() if p >= 0)

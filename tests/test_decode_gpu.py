@@ -1,0 +1,204 @@
+"""K2..K6 decode-layer parity on the device: against decode runs of the
+reference itself (golden fixtures) and against the pinned oracle on seeded
+inputs (C1 geometry, GQA, per-kv-head scope).
+
+Tolerances (north star): outputs within 2e-3 relative -- the norm-relative
+error per (seq, row, q head) of the bf16 device output against the reference
+output rounded to bf16 (bf16 I/O), plus an elementwise bound of 4e-3 * max|O|;
+agg / pinned mass to 1e-4 relative (fp32 accumulation order); top-k sets
+identical except where the reference's own scores at the k / k+1 boundary
+are within 1e-4 relative (documented near-tie band)."""
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import restate as R
+from oracle.synth import make_kv, make_queries, make_step_kv
+
+pytestmark = pytest.mark.gpu
+
+OUT_RTOL = 2e-3
+TIE_BAND = 1e-4
+
+
+def _dec(cache):
+    from paper_2503_16163_b200 import SpeculativeLayerDecoder
+    return SpeculativeLayerDecoder(cache)
+
+
+def assert_out_close(got, exp):
+    """bf16 I/O: the device output is compared with the reference output
+    rounded to bf16 (the output rounding is part of the contract)."""
+    got = np.asarray(got, np.float32).reshape(exp.shape[0], -1, exp.shape[-1])
+    exp = exp.reshape(got.shape)
+    exp16 = R.bf16_round(exp)
+    for r in range(exp.shape[0]):
+        for h in range(exp.shape[1]):
+            e = np.linalg.norm(got[r, h] - exp16[r, h]) / max(np.linalg.norm(exp[r, h]), 1e-30)
+            assert e <= OUT_RTOL, f"row {r} head {h}: rel err {e:.2e}"
+    assert np.abs(got - exp).max() <= 4e-3 * np.abs(exp).max()
+
+
+def assert_topk_equivalent(got, exp, agg_ref, k):
+    got, exp = set(got), set(exp)
+    if got == exp:
+        return
+    kth = np.sort(agg_ref[list(exp)])[0] if exp else 0.0
+    for p in got ^ exp:  # every disagreement must sit inside the near-tie band
+        assert abs(agg_ref[p] - kth) <= TIE_BAND * max(kth, 1e-30), (p, agg_ref[p], kth)
+
+
+@pytest.mark.parametrize("impl", ["auto", "generic"])
+@pytest.mark.parametrize("tag", ["mha_b2", "gqa_b1", "mha_b16", "gqa4_b2"])
+def test_decode_layer_matches_reference_run(tag, impl):
+    import torch
+    from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
+    z = golden(f"decode_{tag}.npz")
+    bits, g, r, k, Hq = (int(z[x]) for x in ("bits", "g", "r", "k", "Hq"))
+    K0, V0 = z["K0"], z["V0"]
+    n0, H, d = K0.shape
+    steps = int(z["steps"])
+    budget = CacheBudget(bits=bits, group_size=g, residual=r, prefetch_k=k, context_length=n0 + steps + 8)
+    cache = DeviceTwoTierCache(1, H, d, budget, q_heads=Hq)
+    cache.set_attend_impl(impl)
+    cache.prefill(0, K0[None], V0[None])
+    dec = _dec(cache)
+    out = dec.predecode_layer(0, z["pre_q"][None], z["pre_k"][None], z["pre_v"][None])
+    assert_out_close(out[0].float().cpu().numpy(), z["pre_out"])
+    picked, newc = dec.ticket(0)
+    f0 = R.frontier(n0, r, g)
+    agg = dec.debug_agg(0)[0, 0, :f0].cpu().numpy()
+    np.testing.assert_allclose(agg, z["pre_agg"][:f0], rtol=1e-4, atol=1e-7)
+    got = [p for p in picked[0, 0].tolist() if p >= 0]
+    assert_topk_equivalent(got, z["pre_picked"].tolist(), z["pre_agg"], k)
+    prev = set(z["pre_picked"].tolist())
+    for i in range(steps):
+        res = dec.decode_layer(0, i + 1, z["q"][i][None], z["k_new"][i][None], z["v_new"][i][None])
+        torch.cuda.synchronize()
+        assert_out_close(res.out[0].float().cpu().numpy(), z["out"][i])
+        np.testing.assert_allclose(res.pinned_mass[0].cpu().numpy(), z["pinned_mass"][i],
+                                   rtol=1e-4, atol=1e-6)
+        n = n0 + i
+        f = R.frontier(n, r, g)
+        agg = dec.debug_agg(0)[0, 0, :f].cpu().numpy()
+        np.testing.assert_allclose(agg, z["agg"][i][:f], rtol=1e-4, atol=1e-7)
+        picked, newc = dec.ticket(0)
+        got = [p for p in picked[0, 0].tolist() if p >= 0]
+        exp = [p for p in z["picked"][i].tolist() if p >= 0]
+        assert_topk_equivalent(got, exp, z["agg"][i], k)
+        if set(got) == set(exp):
+            assert int(newc[0, 0]) == len([p for p in exp if p not in prev])
+        prev = set(got)
+        assert cache.length(0) == n + 1
+    cache.close()
+
+
+def _oracle_run(cfg, seed, steps=3, impl="auto"):
+    """Seeded C1-like run: device vs oracle for predecode + `steps` decode steps."""
+    import torch
+    from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
+    b, n0, H, Hq, d, bits, g, r, k, scope = cfg
+    rng = np.random.default_rng(seed)
+    states, KV = [], []
+    for s in range(b):
+        K, V = make_kv(rng, n0, H, d)
+        st = R.LayerState(H, d, bits, g, r, k, scope)
+        st.extend(K, V)
+        states.append(st)
+        KV.append((K, V))
+    budget = CacheBudget(bits=bits, group_size=g, residual=r, prefetch_k=k, context_length=n0 + steps + 8)
+    cache = DeviceTwoTierCache(1, H, d, budget, batch=b, q_heads=Hq, topk_scope=scope)
+    cache.set_attend_impl(impl)
+    cache.prefill(0, np.stack([x[0] for x in KV]), np.stack([x[1] for x in KV]))
+    dec = _dec(cache)
+    q = np.stack([make_queries(rng, 1, Hq, d) for _ in range(b)])
+    kn, vn = zip(*[make_step_kv(rng, 1, H, d) for _ in range(b)])
+    kn, vn = np.stack(kn), np.stack(vn)
+    out = dec.predecode_layer(0, q, kn, vn).float().cpu().numpy()
+    U = cache.units
+    for s in range(b):
+        o = R.predecode_layer(states[s], q[s], kn[s], vn[s])
+        assert_out_close(out[s], o["out"])
+        picked, _ = dec.ticket(0)
+        for u in range(U):
+            got = [p for p in picked[s, u].tolist() if p >= 0]
+            assert_topk_equivalent(got, list(o["picked"][u]), o["agg"][u], k)
+            states[s].pinned[u] = tuple(sorted(got))   # follow the device's set
+    qcur = np.stack([make_queries(rng, 2, Hq, d) for _ in range(b)])
+    for t in range(1, steps + 1):
+        kn, vn = zip(*[make_step_kv(rng, 2, H, d) for _ in range(b)])
+        kn, vn = np.stack(kn), np.stack(vn)
+        res = dec.decode_layer(0, t, qcur, kn, vn)
+        torch.cuda.synchronize()
+        outs = res.out.float().cpu().numpy()
+        pm = res.pinned_mass.cpu().numpy()
+        picked, newc = dec.ticket(0)
+        for s in range(b):
+            o = R.decode_layer(states[s], qcur[s], kn[s], vn[s])
+            assert_out_close(outs[s], o["out"])
+            np.testing.assert_allclose(pm[s], o["pinned_mass"], rtol=1e-4, atol=1e-6)
+            for u in range(U):
+                got = [p for p in picked[s, u].tolist() if p >= 0]
+                assert_topk_equivalent(got, list(o["picked"][u]), o["agg"][u], k)
+                if set(got) == set(o["picked"][u]):
+                    assert int(newc[s, u]) == len(o["new"][u])
+                states[s].pinned[u] = tuple(sorted(got))
+        qcur = (qcur + 0.3 * rng.standard_normal(qcur.shape)).astype(np.float32)
+        qcur = R.bf16_round(qcur)
+    cache.close()
+
+
+@pytest.mark.parametrize("impl", ["auto", "generic"])
+def test_c1_geometry_vs_oracle(impl):
+    # BASELINE config 1: 32 heads x d=128, ctx 4096, 2-bit, k=64, r=32, batch 1
+    _oracle_run((1, 4096, 32, 32, 128, 2, 32, 32, 64, "layer"), seed=11, impl=impl)
+
+
+@pytest.mark.parametrize("bits", [1, 2])
+def test_gqa_batch_vs_oracle(bits):
+    _oracle_run((3, 1500, 2, 8, 128, bits, 32, 64, 32, "layer"), seed=12 + bits)
+
+
+def test_kv_head_scope_vs_oracle():
+    _oracle_run((2, 1200, 4, 16, 128, 1, 32, 64, 16, "kv_head"), seed=21)
+
+
+def test_select_topk_kats_and_ties():
+    from paper_2503_16163_b200 import select_topk
+    assert select_topk([0.1, 0.9, 0.5], 2) == (1, 2)
+    assert select_topk([0.5, 0.5, 0.5], 2) == (0, 1)
+    assert select_topk([1.0], 0) == ()
+    assert select_topk([0.3, 0.1, 0.2, 0.2, 0.2], 3) == (0, 2, 3)
+    rng = np.random.default_rng(5)
+    for n, k in [(20, 7), (1000, 64), (4096, 64), (131072, 256), (262144, 512), (50, 100)]:
+        s = rng.integers(0, 40, size=n).astype(np.float32) / 40  # heavy ties
+        assert select_topk(s, k) == R.select_topk(s, k, range(n))
+        s = rng.random(n).astype(np.float32)
+        assert select_topk(s, k) == R.select_topk(s, k, range(n))
+
+
+def test_protocol_errors():
+    from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache, ProtocolError
+    rng = np.random.default_rng(6)
+    K, V = make_kv(rng, 100, 2, 128)
+    cache = DeviceTwoTierCache(2, 2, 128, CacheBudget(bits=2, group_size=32, residual=32,
+                                                      prefetch_k=8, context_length=256))
+    for layer in range(2):
+        cache.prefill(layer, K[None], V[None])
+    dec = _dec(cache)
+    q = make_queries(rng, 2, 2, 128)[None]
+    kn, vn = make_step_kv(rng, 2, 2, 128)
+    with pytest.raises(ProtocolError):
+        dec.decode_layer(0, 1, q, kn[None], vn[None])        # no ticket issued at step 0
+    dec.predecode_layer(0, q[:, :1], kn[None, :1], vn[None, :1])
+    with pytest.raises(ProtocolError):
+        dec.predecode_layer(0, q[:, :1], kn[None, :1], vn[None, :1])  # duplicate ticket
+    dec.decode_layer(0, 1, q, kn[None], vn[None])
+    with pytest.raises(ProtocolError):
+        dec.decode_layer(0, 1, q, kn[None], vn[None])        # ticket already awaited
+    with pytest.raises(ProtocolError):
+        dec.decode_layer(1, 1, q, kn[None], vn[None])        # layer 1 never predecoded
+    dec.decode_layer(0, 2, q, kn[None], vn[None])
+    with pytest.raises(ProtocolError):
+        cache.prefill(0, K[None], V[None])                   # prefill may only run once
+    cache.close()
