@@ -150,6 +150,13 @@ SPC_API int spc_export_packed(spc_cache* cache, int layer, int seq, uint8_t* key
  * positions, HOST bf16 outputs [npos][kv_heads][d].  Synchronous. */
 SPC_API int spc_slow_fetch(spc_cache* cache, int layer, int seq, const int32_t* positions, int npos,
                    void* k_out, void* v_out);
+/* Live profiling: synchronizes, returns the CUDA-event time summed over the
+ * K2 attention launches (compute stream) and the K4+K5 ticket work (copy
+ * stream) recorded since the previous call, the number of recorded launches,
+ * and the count of kernels the library launched; then resets and turns
+ * recording on (enable=1) or off. */
+SPC_API int spc_profile(spc_cache* cache, int enable, double* attn_ms, int64_t* attn_launches,
+                        double* sel_ms, int64_t* sel_launches, int64_t* launches);
 /* Device pointer + element count of the pin state of (layer): pin_pos int32
  * [batch][units][k] (-1 = empty slot). */
 SPC_API int spc_pin_state(spc_cache* cache, int layer, const int32_t** pin_pos);

@@ -275,10 +275,13 @@ def select_topk(scores: np.ndarray, k: int, eligible) -> tuple:
 class LayerState:
     """One (layer, sequence) of the reference ``TwoTierCache`` in array form.
 
-    ``append`` follows ``append_verified``/``migrate_residual``
-    (``kvcache.py:162-192``); ``pinned`` follows ``pin`` (``kvcache.py:194-218``,
-    whole-set replacement).  ``pinned`` is a dict unit -> sorted tuple where
-    unit is 0 for the reference's per-layer scope, or the kv head for the
+    ``append``/``extend`` follow ``append_verified``/``migrate_residual``
+    (``kvcache.py:162-192``): blocks crossing the frontier are quantized once
+    and their codes + float64 params are kept (the reference's ``_PackedBlock``
+    list); ``materialize_head`` dequantizes them every call like
+    ``materialize`` (``kvcache.py:222-243``).  ``pinned`` follows ``pin``
+    (``kvcache.py:194-218``, whole-set replacement): a dict unit -> sorted
+    tuple, unit 0 for the reference's per-layer scope, or the kv head for the
     per-(kv-head) extension.
     """
 
@@ -291,6 +294,9 @@ class LayerState:
         self.V = np.zeros((0, kv_heads, head_dim), np.float32)
         nunits = 1 if scope == "layer" else kv_heads
         self.pinned = {u: () for u in range(nunits)}
+        self._pf = 0            # frontier covered by the stored codes
+        self._kq = []           # per block batch: (codes [nb,H,d,g], zero, scale [nb,H,d])
+        self._vq = []           # per token batch: list over chunks of (codes, zero, scale)
 
     @property
     def n(self) -> int:
@@ -311,16 +317,43 @@ class LayerState:
     def unit_of(self, head: int) -> int:
         return 0 if self.scope == "layer" else head
 
-    def materialize(self):
-        """Per-head effective K, V: list over kv heads of ([n,d], [n,d])."""
+    def _sync_packed(self) -> None:
         f = self.f
-        Kt, Vt = materialize_all(self.K, self.V, f, self.bits, self.g)
-        if self.bits != FULL_PRECISION_BITS:
-            for h in range(self.H):
-                for p in self.pinned[self.unit_of(h)]:
-                    Kt[p, h] = self.K[p, h]
-                    Vt[p, h] = self.V[p, h]
-        return ([Kt[:, h, :] for h in range(self.H)], [Vt[:, h, :] for h in range(self.H)])
+        if self.bits == FULL_PRECISION_BITS or f <= self._pf:
+            return
+        a, g, H, d = self._pf, self.g, self.H, self.d
+        nb = (f - a) // g
+        self._kq.append(quantize_keys_block(self.K[a:f].reshape(nb, g, H, d), self.bits))
+        self._vq.append(quantize_values(self.V[a:f], self.bits, g))
+        self._pf = f
+
+    def materialize_head(self, h: int):
+        """Effective K, V [n, d] float32 of kv head h (kvcache.py:222-243)."""
+        self._sync_packed()
+        f = self.f
+        Kt = self.K[:, h, :].copy()
+        Vt = self.V[:, h, :].copy()
+        if self.bits != FULL_PRECISION_BITS and f:
+            pos = 0
+            for (kc, kz, ks), vchunks in zip(self._kq, self._vq):
+                nb = kc.shape[0]
+                rows = nb * self.g
+                Kt[pos:pos + rows] = dequantize(kc[:, h], kz[:, h], ks[:, h]).transpose(0, 2, 1).reshape(rows, self.d)
+                j0 = 0
+                for c, z, sc in vchunks:
+                    w = c.shape[-1]
+                    Vt[pos:pos + rows, j0:j0 + w] = dequantize(c[:, h], z[:, h], sc[:, h])
+                    j0 += w
+                pos += rows
+            for p in self.pinned[self.unit_of(h)]:
+                Kt[p] = self.K[p, h]
+                Vt[p] = self.V[p, h]
+        return Kt, Vt
+
+    def materialize(self):
+        """Per-head effective K, V: lists over kv heads of [n, d]."""
+        ks, vs = zip(*[self.materialize_head(h) for h in range(self.H)])
+        return list(ks), list(vs)
 
 
 def _agg_by_unit(probs, row: int, n: int, group: int, scope: str, kv_heads: int):
@@ -329,6 +362,26 @@ def _agg_by_unit(probs, row: int, n: int, group: int, scope: str, kv_heads: int)
         return [np.sum([a[row, :n] for a in probs], axis=0)]
     return [np.sum([probs[j][row, :n] for j in range(h * group, (h + 1) * group)], axis=0)
             for h in range(kv_heads)]
+
+
+def _attend_streaming(state: LayerState, q: np.ndarray, k_new: np.ndarray, v_new: np.ndarray,
+                      mask: np.ndarray):
+    """``attend`` over [materialize(h) ; in-step rows], one kv head at a time
+    (same float32 arithmetic as engine.py:51-63, bounded memory)."""
+    Hq, d = q.shape[1], q.shape[2]
+    group = Hq // state.H
+    scale = np.float32(d ** -0.5)
+    outs, probs = [None] * Hq, [None] * Hq
+    for h in range(state.H):
+        mk, mv = state.materialize_head(h)
+        keys = np.concatenate([mk, k_new[:, h, :]], 0)
+        vals = np.concatenate([mv, v_new[:, h, :]], 0)
+        for hq in range(h * group, (h + 1) * group):
+            scores = (q[:, hq, :] @ keys.T) * scale
+            a = masked_softmax_rows(scores, mask)
+            outs[hq] = a @ vals
+            probs[hq] = a
+    return np.concatenate(outs, axis=1), probs
 
 
 def decode_layer(state: LayerState, q: np.ndarray, k_new: np.ndarray, v_new: np.ndarray,
@@ -340,15 +393,13 @@ def decode_layer(state: LayerState, q: np.ndarray, k_new: np.ndarray, v_new: np.
     probs (per q head), agg (per unit), picked (per unit), new (per unit),
     pinned_mass [Hq].  Appends row 0 when ``append`` (``engine.py:321``).
     """
+    q = np.asarray(q, np.float32)
     Hq, d = q.shape[1], q.shape[2]
     group = Hq // state.H
     n, f = state.n, state.f
-    mk, mv = state.materialize()
-    keys = [np.concatenate([mk[h], k_new[:, h, :]], 0) for h in range(state.H)]
-    vals = [np.concatenate([mv[h], v_new[:, h, :]], 0) for h in range(state.H)]
     mask = np.ones((2, n + 2), dtype=bool)
     mask[0, n + 1] = False  # engine.py:310
-    out, probs = attend(q, keys, vals, mask, group)
+    out, probs = _attend_streaming(state, q, k_new, v_new, mask)
     pinned_mass = np.zeros(Hq, np.float64)
     for j, a in enumerate(probs):  # engine.py:314-316
         pins = list(state.pinned[state.unit_of(j // group)])
@@ -370,14 +421,12 @@ def predecode_layer(state: LayerState, q: np.ndarray, k_new: np.ndarray, v_new: 
     """One layer of ``SpeculativeDecoder.predecode`` (``engine.py:245-268``):
     single row at position n against the fast tier plus its own KV, agg from
     row 0, no append."""
+    q = np.asarray(q, np.float32)
     Hq, d = q.shape[1], q.shape[2]
     group = Hq // state.H
     n, f = state.n, state.f
-    mk, mv = state.materialize()
-    keys = [np.concatenate([mk[h], k_new[:, h, :]], 0) for h in range(state.H)]
-    vals = [np.concatenate([mv[h], v_new[:, h, :]], 0) for h in range(state.H)]
     mask = np.ones((1, n + 1), dtype=bool)
-    out, probs = attend(q, keys, vals, mask, group)
+    out, probs = _attend_streaming(state, q, k_new, v_new, mask)
     aggs = _agg_by_unit(probs, 0, n, group, state.scope, state.H)
     picked, new = [], []
     for u, agg in enumerate(aggs):

@@ -60,6 +60,12 @@ struct spc_cache {
   float *part_o = nullptr, *part_ml = nullptr, *pin_ml = nullptr, *spill = nullptr, *mz = nullptr;
   int32_t* staging = nullptr;
   int context_length = 0;
+  // live profiling of the dominant kernel (K2) and the copy-stream work (K4+K5)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_attn, prof_sel;
+  int64_t launches = 0;
 };
 
 namespace {
@@ -104,6 +110,7 @@ int migrate(spc_cache* c, int layer, cudaStream_t st) {
   // ring layout is [b][H][ring][d]: row stride d, head stride ring*d
   launch_quantize(G, c->L[layer], S, (int)(c->f[layer] / G.g), 1, st);
   CUDA_TRY(cudaGetLastError());
+  c->launches += 1;
   c->f[layer] += G.g;
   return SPC_OK;
 }
@@ -113,6 +120,7 @@ int append_rows(spc_cache* c, int layer, const void* kr, const void* vr, int64_t
   const Geo& G = c->G;
   if (c->n[layer] >= c->context_length)
     return fail(SPC_EINVAL, "context_length exceeded");
+  c->launches += 1;
   launch_append(G, c->L[layer], (const __nv_bfloat16*)kr, (const __nv_bfloat16*)vr,
                 seq_stride ? seq_stride : (int64_t)G.H * G.d, (int)c->n[layer],
                 host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer), st);
@@ -123,6 +131,15 @@ int append_rows(spc_cache* c, int layer, const void* kr, const void* vr, int64_t
     if (rc) return rc;
   }
   return SPC_OK;
+}
+
+cudaEvent_t prof_event(spc_cache* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
 }
 
 int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_new,
@@ -148,26 +165,47 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
   a.sm_scale_log2 = (float)(1.0 / std::sqrt((double)G.d) * 1.4426950408889634);
   bool fast = (c->impl != 1) && attend_fast_supported(G, rows);
   if (c->impl == 2 && !fast) return fail(SPC_EINVAL, "fast attention path not available for this geometry");
+  cudaEvent_t p0 = nullptr, p1 = nullptr;
+  if (c->prof) {
+    p0 = prof_event(c);
+    p1 = prof_event(c);
+    CUDA_TRY(cudaEventRecord(p0, st));
+  }
   if (fast) {
-    launch_attend_fast(a, st);  // chooses its own split plan
+    c->launches += launch_attend_fast(a, st);  // K2 (+ fused combine); own split plan
   } else {
     choose_splits(c, a.f, &a.nsplit, &a.blocks_per_split);
     launch_attend_generic(a, st);
     CUDA_TRY(cudaGetLastError());
     launch_combine(a, st);
-    CUDA_TRY(cudaGetLastError());
+    c->launches += 2;
   }
   CUDA_TRY(cudaGetLastError());
+  if (c->prof) {
+    CUDA_TRY(cudaEventRecord(p1, st));
+    c->prof_attn.push_back({p0, p1});
+  }
   launch_agg(a, st);
+  c->launches += a.f > 0;
   CUDA_TRY(cudaGetLastError());
   // ticket: selection + prefetch on the copy stream (transfer.py:84-94)
   CUDA_TRY(cudaEventRecord(c->ev_agg[layer], st));
   CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev_agg[layer], 0));
+  if (c->prof) {
+    p0 = prof_event(c);
+    p1 = prof_event(c);
+    CUDA_TRY(cudaEventRecord(p0, c->copy_stream));
+  }
   launch_topk(G, c->L[layer], a.f, c->copy_stream);
   CUDA_TRY(cudaGetLastError());
   launch_prefetch(G, c->L[layer], host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer),
                   c->copy_stream);
+  c->launches += 2;
   CUDA_TRY(cudaGetLastError());
+  if (c->prof) {
+    CUDA_TRY(cudaEventRecord(p1, c->copy_stream));
+    c->prof_sel.push_back({p0, p1});
+  }
   CUDA_TRY(cudaEventRecord(c->ev_pf[layer], c->copy_stream));
   return SPC_OK;
 }
@@ -318,6 +356,7 @@ int spc_cache_destroy(spc_cache* c) {
   for (void* p : c->dev_allocs) cudaFree(p);
   if (c->host_k) cudaFreeHost(c->host_k);
   if (c->host_v) cudaFreeHost(c->host_v);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (auto e : c->ev_agg) if (e) cudaEventDestroy(e);
   for (auto e : c->ev_pf) if (e) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -514,6 +553,35 @@ int spc_slow_fetch(spc_cache* c, int layer, int seq, const int32_t* positions, i
     std::memcpy((char*)k_out + i * row * 2, hk + (size_t)positions[i] * row, row * 2);
     std::memcpy((char*)v_out + i * row * 2, hv + (size_t)positions[i] * row, row * 2);
   }
+  return SPC_OK;
+}
+
+int spc_profile(spc_cache* c, int enable, double* attn_ms, int64_t* attn_launches, double* sel_ms,
+                int64_t* sel_launches, int64_t* launches) {
+  if (!c) return fail(SPC_EINVAL, "null cache");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  double a = 0, s = 0;
+  for (auto& p : c->prof_attn) {
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
+    a += ms;
+  }
+  for (auto& p : c->prof_sel) {
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
+    s += ms;
+  }
+  if (attn_ms) *attn_ms = a;
+  if (attn_launches) *attn_launches = (int64_t)c->prof_attn.size();
+  if (sel_ms) *sel_ms = s;
+  if (sel_launches) *sel_launches = (int64_t)c->prof_sel.size();
+  if (launches) *launches = c->launches;
+  c->prof_attn.clear();
+  c->prof_sel.clear();
+  c->ev_used = 0;
+  c->launches = 0;
+  c->prof = enable != 0;
   return SPC_OK;
 }
 

@@ -4,5 +4,5 @@
 
 namespace spc {
 int attend_fast_supported(const Geo& G, int rows) { return 0; }
-void launch_attend_fast(const AttnArgs& a, cudaStream_t st) {}
+int launch_attend_fast(const AttnArgs& a, cudaStream_t st) { return 0; }
 }  // namespace spc

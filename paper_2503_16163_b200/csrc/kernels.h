@@ -47,7 +47,7 @@ void launch_materialize(const Geo& G, const LayerBufs& B, int b, int h, int n, i
 // K2 (generic exact path and the tensor-core fast path) + K3 combine / agg
 void launch_attend_generic(const AttnArgs& a, cudaStream_t st);
 int attend_fast_supported(const Geo& G, int rows);
-void launch_attend_fast(const AttnArgs& a, cudaStream_t st);
+int launch_attend_fast(const AttnArgs& a, cudaStream_t st);  // returns kernels launched
 void launch_combine(const AttnArgs& a, cudaStream_t st);
 void launch_agg(const AttnArgs& a, cudaStream_t st);
 
