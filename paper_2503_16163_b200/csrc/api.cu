@@ -275,10 +275,11 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
     size_t vpar = G.bits == 16 ? 0 : b * H * G.nblk * (size_t)G.g * G.nch * 4;
     size_t ring = b * H * G.ring * (size_t)G.d * 2;
     size_t pool = b * U * G.k * (size_t)G.Hu * G.d * 2;
-    size_t off[16], tot = 0, sizes[15] = {codes, codes, kpar, vpar, ring, ring, pool, pool,
+    size_t off[16], tot = 0, sizes[16] = {codes, codes, kpar, vpar, ring, ring, pool, pool,
                                           b * U * G.k * 4, b * U * (G.L / 32) * 4, b * U * (size_t)G.L * 4,
-                                          b * U * G.k * 4, b * U * 4, b * U * G.k * 4, b * U * G.k * 4};
-    for (int i = 0; i < 15; ++i) {
+                                          b * U * G.k * 4, b * U * 4, b * U * G.k * 4, b * U * G.k * 4,
+                                          b * H * 2 * 4};
+    for (int i = 0; i < 16; ++i) {
       off[i] = tot;
       tot += align_up(std::max<size_t>(sizes[i], 16), 256);
     }
@@ -300,8 +301,10 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
     B.newcnt = (int32_t*)(base + off[12]);
     B.fetch_slot = (int32_t*)(base + off[13]);
     B.fetch_pos = (int32_t*)(base + off[14]);
+    B.rmax = (uint32_t*)(base + off[15]);
     if (cudaMemset(B.pin_pos, 0xFF, sizes[8]) != cudaSuccess || cudaMemset(B.bitmap, 0, sizes[9]) != cudaSuccess ||
         cudaMemset(B.sel, 0xFF, sizes[11]) != cudaSuccess || cudaMemset(B.newcnt, 0, sizes[12]) != cudaSuccess ||
+        cudaMemset(B.rmax, 0, sizes[15]) != cudaSuccess ||
         cudaMemset(B.ring_k, 0, ring) != cudaSuccess || cudaMemset(B.ring_v, 0, ring) != cudaSuccess ||
         cudaMemset(B.pool_k, 0, pool) != cudaSuccess || cudaMemset(B.pool_v, 0, pool) != cudaSuccess)
       rc = fail(SPC_ECUDA, "cudaMemset failed");

@@ -59,6 +59,7 @@ struct LayerBufs {
   int32_t* newcnt;     // [b][U]
   int32_t* fetch_slot; // [b][U][k]
   int32_t* fetch_pos;  // [b][U][k]
+  uint32_t* rmax;      // [b][H][2] max group range (hi-lo) of keys / values, fp32 bits
 };
 
 // ---- element offsets ---------------------------------------------------------

@@ -48,6 +48,12 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
     return;
   }
 
+  __shared__ float s_rk, s_rv;
+  if (tid == 0) {
+    s_rk = 0.f;
+    s_rv = 0.f;
+  }
+  __syncthreads();
   // key groups: one per channel over the block's tokens (quant.py:163-169)
   for (int c = tid; c < d; c += nt) {
     float lo = sk[c], hi = sk[c];
@@ -57,6 +63,7 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
       hi = fmaxf(hi, x);
     }
     B.kparams[bi * d + c] = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+    atomicMax(reinterpret_cast<unsigned*>(&s_rk), __float_as_uint(hi - lo));
     GroupParams p = params_from_minmax((double)lo, (double)hi, G.bits);
     kz[c] = p.zero;
     ks[c] = p.scale;
@@ -73,6 +80,7 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
     }
     B.vparams[bi * (size_t)(g * G.nch) + i] =
         float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+    atomicMax(reinterpret_cast<unsigned*>(&s_rv), __float_as_uint(hi - lo));
     GroupParams p = params_from_minmax((double)lo, (double)hi, G.bits);
     vz[i] = p.zero;
     vs[i] = p.scale;
@@ -82,6 +90,10 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
     wv[i] = 0u;
   }
   __syncthreads();
+  if (tid == 0) {  // per-(seq, head) range maxima: exponent choice of the MMA path
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 2 + 0], __float_as_uint(s_rk));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 2 + 1], __float_as_uint(s_rv));
+  }
   for (int i = tid; i < g * d; i += nt) {
     int t = i / d, c = i - t * d, w, bit;
     GroupParams pk{kz[c], ks[c]};
