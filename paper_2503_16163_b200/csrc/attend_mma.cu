@@ -31,11 +31,13 @@
 // Work split: grid (nsplit + 1, H, batch), 8 warps per CTA.  A CTA streams a
 // contiguous range of 32-token blocks of one (seq, kv head); each warp owns
 // every 8th block and keeps its own online-softmax state; the CTA merges its
-// warps and writes one (m, l, O) partial.  Per block a warp reads 3072 B
-// (2-bit) / 2048 B (1-bit): codes straight into registers (coalesced,
-// prefetched one block ahead), group params via cp.async into a shared-memory
-// double buffer.  The last split runs the exact segment (pinned slots,
-// residual window, in-step rows) with the generic CTA body.
+// warps and writes one (m, l, O) partial.  Per block a warp needs 3072 B
+// (2-bit) / 2048 B (1-bit) -- key codes, value codes, key and value group
+// params, four contiguous segments -- which one elected lane fetches with
+// cp.async.bulk (TMA) into a 3-stage per-warp shared-memory ring tracked by
+// mbarriers, so two blocks are always in flight while the third is computed.
+// The last split is the exact segment (pinned slots, residual window, in-step
+// rows; full-precision bf16 rows, fp32 CUDA-core dot products).
 #include <algorithm>
 
 #include "exact_segment.cuh"
@@ -45,6 +47,7 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
+constexpr int kStages = 3;
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -78,13 +81,36 @@ __device__ __forceinline__ int ceil_log2(float x) {  // x > 0
   return (x > ldexpf(1.f, e)) ? e + 1 : e;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+// ---- TMA bulk copies + mbarriers (per-warp ring) --------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 
 __device__ __forceinline__ float warp_max_g(float v) {  // over lanes sharing lane&3
   v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 4));
@@ -104,16 +130,23 @@ __device__ __forceinline__ float warp_sum_all(float v) {
   return v;
 }
 
-// key-param word of channel c in the swizzled shared copy (conflict-free reads
-// of channels {32t + ks + 8m} by lane (ks, t))
-__device__ __forceinline__ int kpar_swz(int c) { return c ^ ((c >> 5) << 3); }
+template <int BITS>
+struct StageLayout {
+  static constexpr int kc = 0;                 // key codes: 32 rows x 4*BITS words
+  static constexpr int vc = 32 * 4 * BITS;     // value codes (fragment-native)
+  static constexpr int kp = 2 * 32 * 4 * BITS; // key (lo|hi) per channel
+  static constexpr int vp = kp + 128;          // value (lo|hi) per (token, group)
+  static constexpr int words = vp + 128;
+  static constexpr unsigned code_bytes = 32 * 4 * BITS * 4;
+  static constexpr unsigned bytes = words * 4;
+};
 
-template <int NR>
-struct WarpSmem {
-  uint32_t kpar[2][128];   // key (lo|hi) per channel, swizzled, double buffer
-  uint32_t vpar[2][128];   // value (lo|hi) per (token, group)
-  uint4 bk[8][32];         // key B fragments {b0hi, b1hi, b0lo, b1lo}, [ks][lane ^ ks]
-  float P[NR][33];         // probabilities of the block, [row][token]
+template <int BITS, int NR>
+struct __align__(16) WarpSmem {
+  uint4 bk[8][32];                                        // key B fragments, [ks][lane ^ ks]
+  uint32_t stage[kStages][StageLayout<BITS>::words];      // TMA ring
+  float P[NR][33];                                        // block probabilities [row][token]
+  uint64_t bar[kStages];
 };
 
 template <int NR>
@@ -123,36 +156,245 @@ struct MergeSmem {
   float l[kWarps][NR];
 };
 
+// exact segment scratch (split == nsplit CTAs)
 template <int NR>
+struct ExactSmem {
+  static constexpr int CH = 256;
+  float sc[NR][CH];
+  float fac[NR], m[NR], l[NR], pm[NR], pl[NR];
+  int slots[1024];
+  int npin;
+  float o[kWarps][NR][128];
+};
+
+template <int BITS, int NR>
 constexpr size_t fast_smem_bytes() {
-  return sizeof(WarpSmem<NR>) * kWarps > sizeof(MergeSmem<NR>) ? sizeof(WarpSmem<NR>) * kWarps
-                                                                 : sizeof(MergeSmem<NR>);
+  size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps, b = sizeof(MergeSmem<NR>), c = sizeof(ExactSmem<NR>);
+  return a > b ? (a > c ? a : c) : (b > c ? b : c);
+}
+
+// ---- exact segment: pinned slots + residual ring + in-step rows (bf16, exact) ----------
+// 8 warps; a warp scores one row at a time (lane = 4 channels), rows in chunks of
+// 256 with an online softmax; pinned rows first so their (m, l) gives the pinned
+// mass (engine.py:314-316).
+template <int NR>
+__device__ void exact_segment_fast(const AttnArgs& a, const int split, const int h, const int b,
+                                   unsigned char* smem) {
+  const Geo& G = a.G;
+  const LayerBufs& B = a.B;
+  ExactSmem<NR>& ex = *reinterpret_cast<ExactSmem<NR>*>(smem);
+  constexpr int CH = ExactSmem<NR>::CH;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int unit = G.scope ? h : 0, hh = G.scope ? 0 : h;
+  float Qr[NR][4];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const int r = j / G.G, g2 = j - r * G.G;
+    const uint2 w = *reinterpret_cast<const uint2*>(a.q + (((size_t)b * a.rows + r) * G.Hq + h * G.G + g2) * 128 + 4 * lane);
+    const __nv_bfloat162 q01 = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
+    const __nv_bfloat162 q23 = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
+    Qr[j][0] = __low2float(q01) * a.sm_scale_log2;
+    Qr[j][1] = __high2float(q01) * a.sm_scale_log2;
+    Qr[j][2] = __low2float(q23) * a.sm_scale_log2;
+    Qr[j][3] = __high2float(q23) * a.sm_scale_log2;
+  }
+  const int32_t* pp = B.pin_pos + ((size_t)b * G.U + unit) * G.k;
+  if (tid == 0) {
+    int cnt = 0;
+    for (int s = 0; s < G.k; ++s)
+      if (pp[s] >= 0) ex.slots[cnt++] = s;
+    ex.npin = cnt;
+  }
+  if (tid < NR) {
+    ex.m[tid] = -CUDART_INF_F;
+    ex.l[tid] = 0.f;
+    ex.pm[tid] = -CUDART_INF_F;
+    ex.pl[tid] = 0.f;
+  }
+  __syncthreads();
+  const int npin = ex.npin, nres = a.n - a.f, total = npin + nres + a.rows;
+  const int agg_j0 = a.agg_row * G.G;
+  float acc[NR][4];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+
+  auto row_ptr = [&](int it, const __nv_bfloat16*& kr, const __nv_bfloat16*& vr, int& pos, bool& spec) {
+    spec = false;
+    pos = -1;
+    if (it < npin) {
+      const int slot = ex.slots[it];
+      pos = pp[slot];
+      const size_t o = ((((size_t)b * G.U + unit) * G.k + slot) * G.Hu + hh) * 128;
+      kr = B.pool_k + o;
+      vr = B.pool_v + o;
+    } else if (it < npin + nres) {
+      const int p = a.f + (it - npin);
+      const size_t o = (((size_t)b * G.H + h) * G.ring + p % G.ring) * 128;
+      kr = B.ring_k + o;
+      vr = B.ring_v + o;
+    } else {
+      const int r = it - npin - nres;
+      spec = (r == 1);
+      const size_t o = (((size_t)b * a.rows + r) * G.H + h) * 128;
+      kr = a.k_new + o;
+      vr = a.v_new + o;
+    }
+  };
+
+  for (int c0 = 0; c0 < total;) {
+    int cend = min(total, c0 + CH);
+    if (c0 < npin) cend = min(cend, npin);
+    const int count = cend - c0;
+    for (int it = warp; it < count; it += kWarps) {
+      const __nv_bfloat16 *kr, *vr;
+      int pos;
+      bool spec;
+      row_ptr(c0 + it, kr, vr, pos, spec);
+      const uint2 w = *reinterpret_cast<const uint2*>(kr + 4 * lane);
+      const __nv_bfloat162 k01 = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
+      const __nv_bfloat162 k23 = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
+      const float k0 = __low2float(k01), k1 = __high2float(k01), k2 = __low2float(k23), k3 = __high2float(k23);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        float s = fmaf(Qr[j][0], k0, fmaf(Qr[j][1], k1, fmaf(Qr[j][2], k2, Qr[j][3] * k3)));
+        s = warp_sum_all(s);
+        if (lane == j) {
+          const bool m = spec && j < G.G;  // row 0 never sees the speculative column
+          ex.sc[j][it] = m ? -CUDART_INF_F : s;
+          if (pos >= 0 && j >= agg_j0 && j < agg_j0 + G.G)
+            a.spill[((size_t)b * G.Hq + h * G.G + (j - agg_j0)) * G.L + pos] = s;
+        }
+      }
+    }
+    __syncthreads();
+    if (warp < NR) {  // online softmax of row `warp` over the chunk
+      const int j = warp;
+      float mx = -CUDART_INF_F;
+      for (int i = lane; i < count; i += 32) mx = fmaxf(mx, ex.sc[j][i]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float mold = ex.m[j], mnew = fmaxf(mold, mx);
+      float sum = 0.f;
+      for (int i = lane; i < count; i += 32) {
+        const float p = mnew == -CUDART_INF_F ? 0.f : exp2f(ex.sc[j][i] - mnew);
+        ex.sc[j][i] = p;
+        sum += p;
+      }
+      sum = warp_sum_all(sum);
+      __syncwarp();
+      if (lane == 0) {
+        const float f = mold == -CUDART_INF_F ? 0.f : exp2f(mold - mnew);
+        ex.fac[j] = f;
+        ex.m[j] = mnew;
+        ex.l[j] = ex.l[j] * f + sum;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const float f = ex.fac[j];
+      acc[j][0] *= f;
+      acc[j][1] *= f;
+      acc[j][2] *= f;
+      acc[j][3] *= f;
+    }
+    for (int it = warp; it < count; it += kWarps) {
+      const __nv_bfloat16 *kr, *vr;
+      int pos;
+      bool spec;
+      row_ptr(c0 + it, kr, vr, pos, spec);
+      const uint2 w = *reinterpret_cast<const uint2*>(vr + 4 * lane);
+      const __nv_bfloat162 v01 = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
+      const __nv_bfloat162 v23 = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
+      const float v0 = __low2float(v01), v1 = __high2float(v01), v2 = __low2float(v23), v3 = __high2float(v23);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const float p = ex.sc[j][it];
+        acc[j][0] = fmaf(p, v0, acc[j][0]);
+        acc[j][1] = fmaf(p, v1, acc[j][1]);
+        acc[j][2] = fmaf(p, v2, acc[j][2]);
+        acc[j][3] = fmaf(p, v3, acc[j][3]);
+      }
+    }
+    __syncthreads();
+    if (cend == npin && tid < NR) {  // state after the pinned rows only
+      ex.pm[tid] = ex.m[tid];
+      ex.pl[tid] = ex.l[tid];
+    }
+    c0 = cend;
+  }
+#pragma unroll
+  for (int j = 0; j < NR; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ex.o[warp][j][4 * lane + i] = acc[j][i];
+  __syncthreads();
+  const size_t base = (((size_t)b * G.H + h) * (a.nsplit + 1) + split) * NR;
+  for (int i = tid; i < NR * 128; i += kThreads) {
+    const int j = i >> 7, c = i & 127;
+    float o = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) o += ex.o[w][j][c];
+    a.part_o[(base + j) * 128 + c] = o;
+  }
+  if (tid < NR) {
+    a.part_ml[(base + tid) * 2 + 0] = ex.m[tid];
+    a.part_ml[(base + tid) * 2 + 1] = ex.l[tid];
+    const size_t pb = ((size_t)b * G.H + h) * NR + tid;
+    a.pin_ml[pb * 2 + 0] = ex.pm[tid];
+    a.pin_ml[pb * 2 + 1] = ex.pl[tid];
+  }
 }
 
 template <int BITS, int NR>
 __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
-  constexpr bool PG = (NR * 4 <= 8);    // value MMA columns = (group, row) pairs
-  constexpr int KW = BITS * 2;          // key-code words per lane per m-tile (2 tokens x BITS words)
-  constexpr int VW = BITS * 4;          // value-code words per lane per block
+  constexpr bool PG = (NR * 4 <= 8);  // value MMA columns = (group, row) pairs
+  using SL = StageLayout<BITS>;
   const Geo& G = a.G;
   const LayerBufs& B = a.B;
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  if (split == a.nsplit) {  // exact segment: first 128 threads
-    if (threadIdx.x < kCH) generic_cta(a, split, h, b, reinterpret_cast<float*>(smem_raw));
+  if (split == a.nsplit) {
+    exact_segment_fast<NR>(a, split, h, b, smem_raw);
     return;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
-  WarpSmem<NR>& ws = reinterpret_cast<WarpSmem<NR>*>(smem_raw)[warp];
+  WarpSmem<BITS, NR>& ws = reinterpret_cast<WarpSmem<BITS, NR>*>(smem_raw)[warp];
 
   const int nb_total = a.f / 32;
   const int blk0 = split * a.blocks_per_split;
   const int blk1 = min(nb_total, blk0 + a.blocks_per_split);
   const float cs = BITS == 1 ? 0.5f : (1.f / 3.f);
+  const size_t bi0 = blk_index(G, b, h, 0);
+  const uint32_t* kc_base = B.kcodes + bi0 * (size_t)G.bwords;
+  const uint32_t* vc_base = B.vcodes + bi0 * (size_t)G.bwords;
+  const uint32_t* kp_base = B.kparams + bi0 * 128;
+  const uint32_t* vp_base = B.vparams + bi0 * 128;
+  const uint32_t* bm_base = B.bitmap + ((size_t)b * G.U + (G.scope ? h : 0)) * (G.L / 32);
 
-  // ---- per-lane query slice for the cooperative key-B construction ----------------
-  // lane (ks = lane&7, tk = lane>>3) owns channels 32tk + ks + 8m, m = 0..3
+  // ---- TMA ring prologue -------------------------------------------------------------
+  auto issue = [&](int blk, int st) {
+    uint32_t* s = ws.stage[st];
+    mbar_expect_tx(&ws.bar[st], SL::bytes);
+    tma_load(s + SL::kc, kc_base + (size_t)blk * G.bwords, SL::code_bytes, &ws.bar[st]);
+    tma_load(s + SL::vc, vc_base + (size_t)blk * G.bwords, SL::code_bytes, &ws.bar[st]);
+    tma_load(s + SL::kp, kp_base + (size_t)blk * 128, 512, &ws.bar[st]);
+    tma_load(s + SL::vp, vp_base + (size_t)blk * 128, 512, &ws.bar[st]);
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(&ws.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) {
+      const int blk = blk0 + warp + s * kWarps;
+      if (blk < blk1) issue(blk, s);
+    }
+  }
+  __syncwarp();
+
+  // ---- per-lane constants ---------------------------------------------------------------
+  // key-B role: lane (ks = lane&7, tk = lane>>3) owns channels 32tk + ks + 8m, m = 0..3
   const int kks = lane & 7, ktk = lane >> 3;
   float Qr[NR][4];
   float qabs = 0.f;
@@ -172,112 +414,66 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
   const float rv = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 2 + 1]) * cs;
   const int Ek = (qabs * rk > 0.f) ? ceil_log2(qabs * rk) - 14 : 0;
   const int Ev = (rv > 0.f) ? ceil_log2(rv) - 14 : 0;
-  // key-side K-index scale of this lane's channels: 2^(-sp - Ek)
-  const int sp = BITS == 2 ? 2 * (kks & 3) : kks;
-  const float kk_scale = pow2i(-sp - Ek);
-  const float k_out = pow2i(24 + Ek);  // D * k_out = sum_c code * Q * s
+  const int sp = BITS == 2 ? 2 * (kks & 3) : kks;       // K-index (channel) scale of this lane
+  const float kscale = cs * pow2i(-sp - Ek);              // (hi-lo) -> s * 2^(-sp-Ek)
+  const float k_out = pow2i(24 + Ek);                     // D * k_out = sum_c code * Q * s
   const float v_out = pow2i(24 + Ev);
+  // value K-index (token) scales for q = 2ks + khalf: 2^(-sq - Ev)
+  float vscale[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) vscale[q] = cs * pow2i(-(BITS == 2 ? 2 * q : q) - Ev);
+  // spill rows owned by this lane (score rows 2tq, 2tq+1) that feed the aggregate
+  const int agg_j0 = a.agg_row * G.G;
+  const int jr0 = 2 * tq, jr1 = 2 * tq + 1;
+  float* sp0 = (jr0 < NR && jr0 >= agg_j0 && jr0 < agg_j0 + G.G)
+                   ? a.spill + ((size_t)b * G.Hq + h * G.G + (jr0 - agg_j0)) * G.L : nullptr;
+  float* sp1 = (jr1 < NR && jr1 >= agg_j0 && jr1 < agg_j0 + G.G)
+                   ? a.spill + ((size_t)b * G.Hq + h * G.G + (jr1 - agg_j0)) * G.L : nullptr;
 
-  // zero the unused rows of the key-B fragments once
-  for (int i = lane; i < 8 * 32; i += 32) {
-    int ks = i >> 5, l = i & 31;
+  for (int i = lane; i < 8 * 32; i += 32) {  // unused rows of the key-B fragments stay 0
+    const int ks = i >> 5, l = i & 31;
     if ((l >> 2) >= NR) ws.bk[ks][l ^ ks] = make_uint4(0, 0, 0, 0);
   }
 
-  // ---- per-warp running state -------------------------------------------------------
-  // score rows owned by this lane: 2tq, 2tq+1
   float m_run[2] = {-CUDART_INF_F, -CUDART_INF_F};
   float l_run[2] = {0.f, 0.f};
   float dv[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i) dv[i][0] = dv[i][1] = dv[i][2] = dv[i][3] = 0.f;
-  // value zero-point side sums: PG: role (grp, j) = (gq / NR, gq % NR); else j = gq, per grp
   float zacc[PG ? 1 : 4];
 #pragma unroll
   for (int i = 0; i < (PG ? 1 : 4); ++i) zacc[i] = 0.f;
 
-  const size_t bi0 = blk_index(G, b, h, 0);
-  const uint32_t* kc_base = B.kcodes + bi0 * (size_t)G.bwords;
-  const uint32_t* vc_base = B.vcodes + bi0 * (size_t)G.bwords;
-  const uint32_t* kp_base = B.kparams + bi0 * 128;
-  const uint32_t* vp_base = B.vparams + bi0 * 128;
-  const uint32_t* bm_base = B.bitmap + ((size_t)b * G.U + (G.scope ? h : 0)) * (G.L / 32);
-  const int agg_j0 = a.agg_row * G.G;
+  int it = 0;
+  uint32_t bm = 0;
+  if (blk0 + warp < blk1) bm = bm_base[blk0 + warp];
+  for (int blk = blk0 + warp; blk < blk1; blk += kWarps, ++it) {
+    const int st = it % kStages;
+    const uint32_t nbm = (blk + kWarps < blk1) ? bm_base[blk + kWarps] : 0u;
+    mbar_wait(&ws.bar[st], (it / kStages) & 1);
+    const uint32_t* S = ws.stage[st];
 
-  // code registers (current + prefetched)
-  uint32_t kw[2][KW], vw[VW], nkw[2][KW], nvw[VW], bm = 0, nbm = 0;
-
-  auto load_codes = [&](int blk, uint32_t (&k_)[2][KW], uint32_t (&v_)[VW], uint32_t& bm_) {
-    const uint32_t* kc = kc_base + (size_t)blk * G.bwords;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {  // token T0 (half 0) / T1 (half 1)
-        const int T = 16 * mt + gq + 8 * half;
-        if (BITS == 2) {
-          uint2 w = *reinterpret_cast<const uint2*>(kc + T * 8 + 2 * tq);
-          k_[mt][2 * half] = w.x;
-          k_[mt][2 * half + 1] = w.y;
-        } else {
-          k_[mt][half] = kc[T * 4 + tq];
-        }
-      }
-    }
-    const uint32_t* vc = vc_base + (size_t)blk * G.bwords + lane * VW;
-#pragma unroll
-    for (int i = 0; i < VW; i += 4) {
-      uint4 w = *reinterpret_cast<const uint4*>(vc + i);
-      v_[i] = w.x;
-      v_[i + 1] = w.y;
-      v_[i + 2] = w.z;
-      v_[i + 3] = w.w;
-    }
-    bm_ = bm_base[blk];
-  };
-  auto load_params = [&](int blk, int buf) {
-    const int q = lane;  // 16-byte chunk
-    cp_async16(&ws.kpar[buf][4 * (q ^ ((q >> 3) << 1))], kp_base + (size_t)blk * 128 + 4 * q);
-    cp_async16(&ws.vpar[buf][4 * q], vp_base + (size_t)blk * 128 + 4 * q);
-    cp_async_commit();
-  };
-
-  int blk = blk0 + warp;
-  int buf = 0;
-  if (blk < blk1) {
-    load_codes(blk, kw, vw, bm);
-    load_params(blk, 0);
-  }
-  for (; blk < blk1; blk += kWarps, buf ^= 1) {
-    const int nxt = blk + kWarps;
-    if (nxt < blk1) {
-      load_codes(nxt, nkw, nvw, nbm);
-      load_params(nxt, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncwarp();
-
-    // ---- key B fragments (cooperative) + zero-point constants C_j ---------------
+    // ---- key B fragments (cooperative) + zero-point constants C_j -----------------------
     float Cp[NR];
     {
       float s4[4], z4[4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const uint32_t w = ws.kpar[buf][kpar_swz(32 * ktk + kks + 8 * m)];
+        const uint32_t w = S[SL::kp + 32 * ktk + kks + 8 * m];
         const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xFFFF0000u);
-        s4[m] = (hi - lo) * cs * kk_scale;
+        s4[m] = (hi - lo) * kscale;
         z4[m] = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
       }
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        float w0 = Qr[j][0] * s4[0], w1 = Qr[j][1] * s4[1], w2 = Qr[j][2] * s4[2], w3 = Qr[j][3] * s4[3];
+        const float w0 = Qr[j][0] * s4[0], w1 = Qr[j][1] * s4[1], w2 = Qr[j][2] * s4[2],
+                    w3 = Qr[j][3] * s4[3];
         Cp[j] = fmaf(Qr[j][0], z4[0], fmaf(Qr[j][1], z4[1], fmaf(Qr[j][2], z4[2], Qr[j][3] * z4[3])));
         uint4 frag;
         if (BITS == 2) {  // b0 = (m0, m1), b1 = (m2, m3)
           split2(w0, w1, frag.x, frag.z);
           split2(w2, w3, frag.y, frag.w);
-        } else {          // b0 = (m0, m2), b1 = (m1, m3)
+        } else {  // b0 = (m0, m2), b1 = (m1, m3)
           split2(w0, w2, frag.x, frag.z);
           split2(w1, w3, frag.y, frag.w);
         }
@@ -286,12 +482,30 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
 #pragma unroll
       for (int j = 0; j < NR; ++j) Cp[j] = warp_sum_all(Cp[j]);
     }
+    // key codes of this lane's tokens T0 = 16mt + gq, T1 = T0 + 8
+    uint32_t kw[2][2 * BITS];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int T = 16 * mt + gq + 8 * hf;
+        if (BITS == 2) {
+          const uint2 w = *reinterpret_cast<const uint2*>(S + SL::kc + T * 8 + 2 * tq);
+          kw[mt][2 * hf] = w.x;
+          kw[mt][2 * hf + 1] = w.y;
+        } else {
+          kw[mt][hf] = S[SL::kc + T * 4 + tq];
+        }
+      }
+    }
     __syncwarp();
 
-    // ---- scores: D[token][row] over 8 k-steps, 2 m-tiles --------------------------
-    float dk[2][4];
+    // ---- scores: hi and lo chains in separate accumulators ------------------------------
+    float dkh[2][4], dkl[2][4];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) dk[mt][0] = dk[mt][1] = dk[mt][2] = dk[mt][3] = 0.f;
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dkh[mt][i] = dkl[mt][i] = 0.f;
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
       const uint4 bb = ws.bk[ks][lane ^ ks];
@@ -307,19 +521,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
           a3 = (kw[mt][3] >> sh) & msk;
         } else {
           const uint32_t msk = (1u << ks) | (1u << (16 + ks));
-          a0 = kw[mt][0] & msk;          // T0, channels (32tq+ks, +16)
-          a2 = (kw[mt][0] >> 8) & msk;   // T0, channels (32tq+8+ks, +24)
+          a0 = kw[mt][0] & msk;         // T0, channels (32tq+ks, +16)
+          a2 = (kw[mt][0] >> 8) & msk;  // T0, channels (32tq+8+ks, +24)
           a1 = kw[mt][1] & msk;
           a3 = (kw[mt][1] >> 8) & msk;
         }
-        mma16816(dk[mt], a0, a1, a2, a3, bb.x, bb.y);
-        mma16816(dk[mt], a0, a1, a2, a3, bb.z, bb.w);
+        mma16816(dkh[mt], a0, a1, a2, a3, bb.x, bb.y);
+        mma16816(dkl[mt], a0, a1, a2, a3, bb.z, bb.w);
       }
     }
 
-    // ---- epilogue: log2 scores, mask, spill, online softmax ----------------------
-    // lane holds rows jr0 = 2tq, jr1 = 2tq+1 for tokens T = 16mt + gq (+8)
-    const int jr0 = 2 * tq, jr1 = 2 * tq + 1;
+    // ---- epilogue: log2 scores, mask, spill, online softmax -----------------------------
     float c0 = 0.f, c1 = 0.f;
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
@@ -334,13 +546,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
       for (int hf = 0; hf < 2; ++hf) {
         const int T = 16 * mt + gq + 8 * hf;
         const bool msk = (bm >> T) & 1u;
-        sc[mt][2 * hf] = msk ? -CUDART_INF_F : fmaf(dk[mt][2 * hf], k_out, c0);
-        sc[mt][2 * hf + 1] = msk ? -CUDART_INF_F : fmaf(dk[mt][2 * hf + 1], k_out, c1);
+        const float s0 = fmaf(dkh[mt][2 * hf] + dkl[mt][2 * hf], k_out, c0);
+        const float s1 = fmaf(dkh[mt][2 * hf + 1] + dkl[mt][2 * hf + 1], k_out, c1);
+        sc[mt][2 * hf] = msk ? -CUDART_INF_F : s0;
+        sc[mt][2 * hf + 1] = msk ? -CUDART_INF_F : s1;
         if (!msk) {
-          if (jr0 < NR && jr0 >= agg_j0 && jr0 < agg_j0 + G.G)
-            a.spill[((size_t)b * G.Hq + h * G.G + (jr0 - agg_j0)) * G.L + pos0 + T] = sc[mt][2 * hf];
-          if (jr1 < NR && jr1 >= agg_j0 && jr1 < agg_j0 + G.G)
-            a.spill[((size_t)b * G.Hq + h * G.G + (jr1 - agg_j0)) * G.L + pos0 + T] = sc[mt][2 * hf + 1];
+          if (sp0) sp0[pos0 + T] = s0;
+          if (sp1) sp1[pos0 + T] = s1;
         }
       }
     }
@@ -349,28 +561,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     mx0 = warp_max_g(mx0);
     mx1 = warp_max_g(mx1);
     const float mn0 = fmaxf(m_run[0], mx0), mn1 = fmaxf(m_run[1], mx1);
-    const bool grow = (mn0 > m_run[0]) || (mn1 > m_run[1]);
-    if (__any_sync(0xffffffffu, grow)) {
+    if (__any_sync(0xffffffffu, (mn0 > m_run[0]) || (mn1 > m_run[1]))) {
       const float al0 = m_run[0] == -CUDART_INF_F ? 0.f : exp2f(m_run[0] - mn0);
       const float al1 = m_run[1] == -CUDART_INF_F ? 0.f : exp2f(m_run[1] - mn1);
       l_run[0] *= al0;
       l_run[1] *= al1;
-      // alpha for the value accumulator columns of this lane and its z role
-      float ac0, ac1, az[PG ? 1 : 4];
+      float ac0, ac1, az;
       if (PG) {
-        // columns n = 2tq, 2tq+1 -> row n % NR; rows 0..NR-1 live in lanes with tq = 0
+        // value columns n = 2tq, 2tq+1 -> row n % NR; rows 0..1 live in lane 0
         const float r0 = __shfl_sync(0xffffffffu, al0, 0), r1 = __shfl_sync(0xffffffffu, al1, 0);
-        ac0 = NR == 1 ? r0 : r0;  // n = 2tq  -> row (2tq) % NR = 0 for NR in {1, 2}
-        ac1 = NR == 1 ? r0 : r1;  // n = 2tq+1 -> row 0 (NR=1) or 1 (NR=2)
-        az[0] = (NR == 1 || (gq & 1) == 0) ? r0 : r1;
+        ac0 = r0;
+        ac1 = NR == 1 ? r0 : r1;
+        az = (NR == 1 || (gq & 1) == 0) ? r0 : r1;
       } else {
         ac0 = al0;
         ac1 = al1;
-        // z role row j = gq lives in lane (tq = gq >> 1) component gq & 1
         const float x0 = __shfl_sync(0xffffffffu, al0, gq >> 1), x1 = __shfl_sync(0xffffffffu, al1, gq >> 1);
-        const float ar = (gq & 1) ? x1 : x0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) az[i] = ar;
+        az = (gq & 1) ? x1 : x0;
       }
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
@@ -380,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         dv[mt][3] *= ac1;
       }
 #pragma unroll
-      for (int i = 0; i < (PG ? 1 : 4); ++i) zacc[i] *= az[i];
+      for (int i = 0; i < (PG ? 1 : 4); ++i) zacc[i] *= az;
       m_run[0] = mn0;
       m_run[1] = mn1;
     }
@@ -399,14 +606,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     }
     __syncwarp();
 
-    // ---- value B fragments -------------------------------------------------------
-    // lane role: PG: column n = gq -> (grp = gq / NR, row = gq % NR); else row = gq
+    // ---- value B fragments -------------------------------------------------------------
+    // PG: lane column n = gq -> (grp = gq / NR, row = gq % NR); else row = gq, per group
     uint32_t vb[PG ? 1 : 4][2][4];  // [grp][ks] {b0hi, b1hi, b0lo, b1lo}
 #pragma unroll
     for (int gi = 0; gi < (PG ? 1 : 4); ++gi) {
       const int grp = PG ? (gq / NR) : gi;
       const int row = PG ? (gq % NR) : gq;
       const bool live = PG ? (gq < 4 * NR) : (gq < NR);
+      const int prow = (PG || NR == 8) ? row : (row < NR ? row : 0);
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
         float x[4];
@@ -414,25 +622,39 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         for (int slot = 0; slot < 4; ++slot) {
           const int khalf = slot >> 1;
           const int t = 16 * ks + 2 * tq + (slot & 1) + 8 * khalf;
-          const int q = 2 * ks + khalf;
-          const int sq = BITS == 2 ? 2 * q : q;
-          float val = 0.f;
-          if (live) {
-            const uint32_t w = ws.vpar[buf][t * 4 + grp];
-            const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xFFFF0000u);
-            const float p = ws.P[row < NR ? row : 0][t];
-            const float z = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
-            zacc[gi] = fmaf(p, z, zacc[gi]);
-            val = p * ((hi - lo) * cs) * pow2i(-sq - Ev);
-          }
-          x[slot] = val;
+          const uint32_t w = S[SL::vp + t * 4 + grp];
+          const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xFFFF0000u);
+          const float p = live ? ws.P[prow][t] : 0.f;
+          const float z = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
+          zacc[gi] = fmaf(p, z, zacc[gi]);
+          x[slot] = p * (hi - lo) * vscale[2 * ks + khalf];
         }
         split2(x[0], x[1], vb[gi][ks][0], vb[gi][ks][2]);
         split2(x[2], x[3], vb[gi][ks][1], vb[gi][ks][3]);
       }
     }
+    // value codes of this lane
+    uint32_t vw[4 * BITS];
+    if (BITS == 2) {
+      const uint4 w0 = *reinterpret_cast<const uint4*>(S + SL::vc + lane * 4);
+      const uint4 w1 = *reinterpret_cast<const uint4*>(S + SL::vc + 128 + lane * 4);
+      vw[0] = w0.x; vw[1] = w0.y; vw[2] = w0.z; vw[3] = w0.w;
+      vw[4 % (4 * BITS)] = w1.x; vw[5 % (4 * BITS)] = w1.y; vw[6 % (4 * BITS)] = w1.z; vw[7 % (4 * BITS)] = w1.w;
+    } else {
+      const uint4 w0 = *reinterpret_cast<const uint4*>(S + SL::vc + lane * 4);
+      vw[0] = w0.x; vw[1] = w0.y; vw[2] = w0.z; vw[3] = w0.w;
+    }
+    __syncwarp();
+    // the stage is consumed: refill it with block it + kStages (async proxy after generic reads)
+    if (lane == 0) {
+      const int nblk = blk + kStages * kWarps;
+      if (nblk < blk1) {
+        fence_proxy_async();
+        issue(nblk, st);
+      }
+    }
 
-    // ---- P.V over 8 channel m-tiles x 2 token k-steps -----------------------------
+    // ---- P.V over 8 channel m-tiles x 2 token k-steps -------------------------------------
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
 #pragma unroll
@@ -440,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         uint32_t a0, a1, a2, a3;
         const int q0 = 2 * ks, q1 = 2 * ks + 1;
         if (BITS == 2) {
-          const uint32_t W = vw[mt], W8 = W >> 8;
+          const uint32_t W = vw[mt % (4 * BITS)], W8 = W >> 8;
           const uint32_t m0 = (3u << (2 * q0)) | (3u << (16 + 2 * q0));
           const uint32_t m1 = (3u << (2 * q1)) | (3u << (16 + 2 * q1));
           a0 = W & m0;
@@ -448,7 +670,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
           a2 = W & m1;
           a3 = W8 & m1;
         } else {
-          const uint32_t W = vw[mt >> 1] >> (8 * (mt & 1)), W4 = W >> 4;
+          const uint32_t W = vw[(mt >> 1) % (4 * BITS)] >> (8 * (mt & 1)), W4 = W >> 4;
           const uint32_t m0 = (1u << q0) | (1u << (16 + q0));
           const uint32_t m1 = (1u << q1) | (1u << (16 + q1));
           a0 = W & m0;
@@ -461,19 +683,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         mma16816(dv[mt], a0, a1, a2, a3, vb[gi][ks][2], vb[gi][ks][3]);
       }
     }
-
-    // rotate prefetched registers
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int i = 0; i < KW; ++i) kw[mt][i] = nkw[mt][i];
-#pragma unroll
-    for (int i = 0; i < VW; ++i) vw[i] = nvw[i];
     bm = nbm;
-    __syncwarp();
   }
 
   // ---- warp results -> shared, CTA merge -> partial ----------------------------------
+  __syncwarp();
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&ws.bar[s])) : "memory");
+  }
   l_run[0] = warp_sum_g(l_run[0]);
   l_run[1] = warp_sum_g(l_run[1]);
 #pragma unroll
@@ -559,15 +778,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
 
 template <int BITS, int NR>
 void launch_fast_t(const AttnArgs& a, cudaStream_t st) {
-  constexpr size_t smem = fast_smem_bytes<NR>();
+  constexpr size_t smem = fast_smem_bytes<BITS, NR>();
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_attend_fast<BITS, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max(smem, generic_smem_bytes(a.G, a.rows)));
+    cudaFuncSetAttribute(k_attend_fast<BITS, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   dim3 grid(a.nsplit + 1, a.G.H, a.G.batch);
-  k_attend_fast<BITS, NR><<<grid, kThreads, std::max(smem, generic_smem_bytes(a.G, a.rows)), st>>>(a);
+  k_attend_fast<BITS, NR><<<grid, kThreads, smem, st>>>(a);
 }
 
 }  // namespace

@@ -8,7 +8,7 @@
 //                                         group is a column of this block)
 //   vcodes  uint32 [b][H][nblk][g*vrw]    value codes; token-major rows in the
 //                                         generic layout, MMA-fragment-native in
-//                                         the fast layout (see fast_vloc)
+//                                         the fast layout (see vloc)
 //   kparams uint32 [b][H][nblk][d]        bf16 (lo | hi<<16) per key group
 //   vparams uint32 [b][H][nblk][g][nch]   bf16 (lo | hi<<16) per value group
 //   ring_k/v bf16  [b][H][r+g][d]         residual window, slot = pos % (r+g)
@@ -181,7 +181,7 @@ __host__ __device__ inline void vloc(const Geo& G, int t, int c, int* word, int*
   int ks = t >> 4, kk = t & 15, khalf = kk >> 3, kr = kk & 7, tq = kr >> 1, odd = kr & 1;
   int lane = 4 * gq + tq, q = 2 * ks + khalf;
   if (G.bits == 2) {
-    *word = lane * 8 + mt;
+    *word = (mt >> 2) * 128 + lane * 4 + (mt & 3);  // two 512-byte halves: 16 B per lane each
     *bit = 16 * odd + 2 * (4 * rh + q);
   } else {
     *word = lane * 4 + (mt >> 1);
