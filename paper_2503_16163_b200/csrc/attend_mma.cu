@@ -347,7 +347,12 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
 
 template <int BITS, int NR>
 __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
-  constexpr bool PG = (NR * 4 <= 8);  // value MMA columns = (group, row) pairs
+  // PACK: score MMA columns n = 2*row + plane (hi/lo of each row side by side),
+  //       one MMA per k-step and one score row per lane (row = lane & 3).
+  // PG:   P.V columns n = group*NR + row, one B fragment for all value groups.
+  constexpr bool PACK = (2 * NR <= 8);
+  constexpr bool PG = (NR * 4 <= 8);
+  constexpr int RPL = PACK ? 1 : 2;  // score rows per lane
   using SL = StageLayout<BITS>;
   const Geo& G = a.G;
   const LayerBufs& B = a.B;
@@ -418,31 +423,45 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
   const float kscale = cs * pow2i(-sp - Ek);              // (hi-lo) -> s * 2^(-sp-Ek)
   const float k_out = pow2i(24 + Ek);                     // D * k_out = sum_c code * Q * s
   const float v_out = pow2i(24 + Ev);
-  // value K-index (token) scales for q = 2ks + khalf: 2^(-sq - Ev)
-  float vscale[4];
+  float vscale[4];  // value K-index (token) scales, q = 2ks + khalf
 #pragma unroll
   for (int q = 0; q < 4; ++q) vscale[q] = cs * pow2i(-(BITS == 2 ? 2 * q : q) - Ev);
-  // spill rows owned by this lane (score rows 2tq, 2tq+1) that feed the aggregate
+  // score rows of this lane and their spill rows (aggregate source)
   const int agg_j0 = a.agg_row * G.G;
-  const int jr0 = 2 * tq, jr1 = 2 * tq + 1;
-  float* sp0 = (jr0 < NR && jr0 >= agg_j0 && jr0 < agg_j0 + G.G)
-                   ? a.spill + ((size_t)b * G.Hq + h * G.G + (jr0 - agg_j0)) * G.L : nullptr;
-  float* sp1 = (jr1 < NR && jr1 >= agg_j0 && jr1 < agg_j0 + G.G)
-                   ? a.spill + ((size_t)b * G.Hq + h * G.G + (jr1 - agg_j0)) * G.L : nullptr;
+  int jr[RPL];
+  float* spr[RPL];
+#pragma unroll
+  for (int e = 0; e < RPL; ++e) {
+    jr[e] = PACK ? tq : 2 * tq + e;
+    spr[e] = (jr[e] < NR && jr[e] >= agg_j0 && jr[e] < agg_j0 + G.G)
+                 ? a.spill + ((size_t)b * G.Hq + h * G.G + (jr[e] - agg_j0)) * G.L : nullptr;
+  }
 
   for (int i = lane; i < 8 * 32; i += 32) {  // unused rows of the key-B fragments stay 0
     const int ks = i >> 5, l = i & 31;
     if ((l >> 2) >= NR) ws.bk[ks][l ^ ks] = make_uint4(0, 0, 0, 0);
   }
 
-  float m_run[2] = {-CUDART_INF_F, -CUDART_INF_F};
-  float l_run[2] = {0.f, 0.f};
+  float m_run[RPL], l_run[RPL];
+#pragma unroll
+  for (int e = 0; e < RPL; ++e) {
+    m_run[e] = -CUDART_INF_F;
+    l_run[e] = 0.f;
+  }
   float dv[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i) dv[i][0] = dv[i][1] = dv[i][2] = dv[i][3] = 0.f;
   float zacc[PG ? 1 : 4];
 #pragma unroll
   for (int i = 0; i < (PG ? 1 : 4); ++i) zacc[i] = 0.f;
+
+  // alpha (softmax rescale) of score row j as seen from any lane
+  auto alpha_of_row = [&](const float (&al)[RPL], int j) -> float {
+    if (PACK) return __shfl_sync(0xffffffffu, al[0], j & 3);
+    const float x0 = __shfl_sync(0xffffffffu, al[0], (j >> 1) & 3);
+    const float x1 = __shfl_sync(0xffffffffu, al[RPL - 1], (j >> 1) & 3);
+    return (j & 1) ? x1 : x0;
+  };
 
   int it = 0;
   uint32_t bm = 0;
@@ -456,11 +475,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     // ---- key B fragments (cooperative) + zero-point constants C_j -----------------------
     float Cp[NR];
     {
+      const uint4 kp4 = *reinterpret_cast<const uint4*>(S + SL::kp + 4 * lane);
+      const uint32_t kpw[4] = {kp4.x, kp4.y, kp4.z, kp4.w};
       float s4[4], z4[4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const uint32_t w = S[SL::kp + 32 * ktk + kks + 8 * m];
-        const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xFFFF0000u);
+        const float lo = __uint_as_float(kpw[m] << 16), hi = __uint_as_float(kpw[m] & 0xFFFF0000u);
         s4[m] = (hi - lo) * kscale;
         z4[m] = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
       }
@@ -469,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         const float w0 = Qr[j][0] * s4[0], w1 = Qr[j][1] * s4[1], w2 = Qr[j][2] * s4[2],
                     w3 = Qr[j][3] * s4[3];
         Cp[j] = fmaf(Qr[j][0], z4[0], fmaf(Qr[j][1], z4[1], fmaf(Qr[j][2], z4[2], Qr[j][3] * z4[3])));
-        uint4 frag;
+        uint4 frag;  // {b0hi, b1hi, b0lo, b1lo} of row j for fragment lane (j, tk)
         if (BITS == 2) {  // b0 = (m0, m1), b1 = (m2, m3)
           split2(w0, w1, frag.x, frag.z);
           split2(w2, w3, frag.y, frag.w);
@@ -500,15 +520,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     }
     __syncwarp();
 
-    // ---- scores: hi and lo chains in separate accumulators ------------------------------
-    float dkh[2][4], dkl[2][4];
+    // ---- scores -------------------------------------------------------------------------
+    float dk[2][4], dl[2][4];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) dkh[mt][i] = dkl[mt][i] = 0.f;
+      for (int i = 0; i < 4; ++i) dk[mt][i] = dl[mt][i] = 0.f;
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
-      const uint4 bb = ws.bk[ks][lane ^ ks];
+      uint32_t b0, b1, b2 = 0, b3 = 0;
+      if (PACK) {  // column n = gq = 2*row + plane
+        const uint2 bb = reinterpret_cast<const uint2*>(&ws.bk[ks][(4 * (gq >> 1) + tq) ^ ks])[gq & 1];
+        b0 = bb.x;
+        b1 = bb.y;
+      } else {
+        const uint4 bb = ws.bk[ks][lane ^ ks];
+        b0 = bb.x;
+        b1 = bb.y;
+        b2 = bb.z;
+        b3 = bb.w;
+      }
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         uint32_t a0, a1, a2, a3;
@@ -526,19 +557,28 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
           a1 = kw[mt][1] & msk;
           a3 = (kw[mt][1] >> 8) & msk;
         }
-        mma16816(dkh[mt], a0, a1, a2, a3, bb.x, bb.y);
-        mma16816(dkl[mt], a0, a1, a2, a3, bb.z, bb.w);
+        // PACK: hi/lo split over k-step parity into two independent chains
+        if (PACK) {
+          if (ks & 1) mma16816(dl[mt], a0, a1, a2, a3, b0, b1);
+          else mma16816(dk[mt], a0, a1, a2, a3, b0, b1);
+        } else {
+          mma16816(dk[mt], a0, a1, a2, a3, b0, b1);
+          mma16816(dl[mt], a0, a1, a2, a3, b2, b3);
+        }
       }
     }
 
-    // ---- epilogue: log2 scores, mask, spill, online softmax -----------------------------
-    float c0 = 0.f, c1 = 0.f;
+    // ---- epilogue: log2 scores, mask, spill, online softmax ----------------------------
+    float cr[RPL];
 #pragma unroll
-    for (int j = 0; j < NR; ++j) {
-      if (j == jr0) c0 = Cp[j];
-      if (j == jr1) c1 = Cp[j];
+    for (int e = 0; e < RPL; ++e) {
+      cr[e] = 0.f;
+#pragma unroll
+      for (int j = 0; j < NR; ++j)
+        if (j == jr[e]) cr[e] = Cp[j];
     }
-    float sc[2][4];
+    // sc[mt][hf][e]: token T = 16mt + gq + 8hf, row jr[e]
+    float sc[2][2][RPL];
     const int pos0 = blk * 32;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
@@ -546,75 +586,82 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
       for (int hf = 0; hf < 2; ++hf) {
         const int T = 16 * mt + gq + 8 * hf;
         const bool msk = (bm >> T) & 1u;
-        const float s0 = fmaf(dkh[mt][2 * hf] + dkl[mt][2 * hf], k_out, c0);
-        const float s1 = fmaf(dkh[mt][2 * hf + 1] + dkl[mt][2 * hf + 1], k_out, c1);
-        sc[mt][2 * hf] = msk ? -CUDART_INF_F : s0;
-        sc[mt][2 * hf + 1] = msk ? -CUDART_INF_F : s1;
-        if (!msk) {
-          if (sp0) sp0[pos0 + T] = s0;
-          if (sp1) sp1[pos0 + T] = s1;
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) {
+          float d;
+          if (PACK) d = (dk[mt][2 * hf] + dl[mt][2 * hf]) + (dk[mt][2 * hf + 1] + dl[mt][2 * hf + 1]);
+          else d = dk[mt][2 * hf + e] + dl[mt][2 * hf + e];
+          const float s = fmaf(d, k_out, cr[e]);
+          sc[mt][hf][e] = msk ? -CUDART_INF_F : s;
+          if (!msk && spr[e]) spr[e][pos0 + T] = s;
         }
       }
     }
-    float mx0 = fmaxf(fmaxf(sc[0][0], sc[0][2]), fmaxf(sc[1][0], sc[1][2]));
-    float mx1 = fmaxf(fmaxf(sc[0][1], sc[0][3]), fmaxf(sc[1][1], sc[1][3]));
-    mx0 = warp_max_g(mx0);
-    mx1 = warp_max_g(mx1);
-    const float mn0 = fmaxf(m_run[0], mx0), mn1 = fmaxf(m_run[1], mx1);
-    if (__any_sync(0xffffffffu, (mn0 > m_run[0]) || (mn1 > m_run[1]))) {
-      const float al0 = m_run[0] == -CUDART_INF_F ? 0.f : exp2f(m_run[0] - mn0);
-      const float al1 = m_run[1] == -CUDART_INF_F ? 0.f : exp2f(m_run[1] - mn1);
-      l_run[0] *= al0;
-      l_run[1] *= al1;
-      float ac0, ac1, az;
+    float mn[RPL];
+    bool grow = false;
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) {
+      float mx = fmaxf(fmaxf(sc[0][0][e], sc[0][1][e]), fmaxf(sc[1][0][e], sc[1][1][e]));
+      mx = warp_max_g(mx);
+      mn[e] = fmaxf(m_run[e], mx);
+      grow |= mn[e] > m_run[e];
+    }
+    if (__any_sync(0xffffffffu, grow)) {
+      float al[RPL];
+#pragma unroll
+      for (int e = 0; e < RPL; ++e) {
+        al[e] = m_run[e] == -CUDART_INF_F ? 0.f : exp2f(m_run[e] - mn[e]);
+        l_run[e] *= al[e];
+        m_run[e] = mn[e];
+      }
+      // value accumulator columns n = 2tq + e' and the z role of this lane
+      float ac[2], az;
       if (PG) {
-        // value columns n = 2tq, 2tq+1 -> row n % NR; rows 0..1 live in lane 0
-        const float r0 = __shfl_sync(0xffffffffu, al0, 0), r1 = __shfl_sync(0xffffffffu, al1, 0);
-        ac0 = r0;
-        ac1 = NR == 1 ? r0 : r1;
-        az = (NR == 1 || (gq & 1) == 0) ? r0 : r1;
+        ac[0] = alpha_of_row(al, (2 * tq) % NR);
+        ac[1] = alpha_of_row(al, (2 * tq + 1) % NR);
+        az = alpha_of_row(al, gq % NR);
       } else {
-        ac0 = al0;
-        ac1 = al1;
-        const float x0 = __shfl_sync(0xffffffffu, al0, gq >> 1), x1 = __shfl_sync(0xffffffffu, al1, gq >> 1);
-        az = (gq & 1) ? x1 : x0;
+        ac[0] = alpha_of_row(al, 2 * tq);
+        ac[1] = alpha_of_row(al, 2 * tq + 1);
+        az = alpha_of_row(al, gq);
       }
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
-        dv[mt][0] *= ac0;
-        dv[mt][1] *= ac1;
-        dv[mt][2] *= ac0;
-        dv[mt][3] *= ac1;
+        dv[mt][0] *= ac[0];
+        dv[mt][1] *= ac[1];
+        dv[mt][2] *= ac[0];
+        dv[mt][3] *= ac[1];
       }
 #pragma unroll
       for (int i = 0; i < (PG ? 1 : 4); ++i) zacc[i] *= az;
-      m_run[0] = mn0;
-      m_run[1] = mn1;
     }
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         const int T = 16 * mt + gq + 8 * hf;
-        const float p0 = exp2f(sc[mt][2 * hf] - m_run[0]);
-        const float p1 = exp2f(sc[mt][2 * hf + 1] - m_run[1]);
-        l_run[0] += p0;
-        l_run[1] += p1;
-        if (jr0 < NR) ws.P[jr0][T] = p0;
-        if (jr1 < NR) ws.P[jr1][T] = p1;
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) {
+          const float p = exp2f(sc[mt][hf][e] - m_run[e]);
+          l_run[e] += p;
+          if (jr[e] < NR) ws.P[jr[e]][T] = p;
+        }
       }
     }
     __syncwarp();
 
-    // ---- value B fragments -------------------------------------------------------------
+    // ---- value B fragments (single f16 plane) -------------------------------------------
     // PG: lane column n = gq -> (grp = gq / NR, row = gq % NR); else row = gq, per group
-    uint32_t vb[PG ? 1 : 4][2][4];  // [grp][ks] {b0hi, b1hi, b0lo, b1lo}
+    uint32_t vb[PG ? 1 : 4][2][2];  // [grp][ks] {b0, b1}
 #pragma unroll
     for (int gi = 0; gi < (PG ? 1 : 4); ++gi) {
       const int grp = PG ? (gq / NR) : gi;
       const int row = PG ? (gq % NR) : gq;
       const bool live = PG ? (gq < 4 * NR) : (gq < NR);
-      const int prow = (PG || NR == 8) ? row : (row < NR ? row : 0);
+      const int prow = row < NR ? row : 0;
+      const uint4 v0 = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * grp + 8 * tq);
+      const uint4 v1 = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * grp + 8 * tq + 4);
+      const uint32_t vpw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};  // [ks][slot]
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
         float x[4];
@@ -622,27 +669,32 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         for (int slot = 0; slot < 4; ++slot) {
           const int khalf = slot >> 1;
           const int t = 16 * ks + 2 * tq + (slot & 1) + 8 * khalf;
-          const uint32_t w = S[SL::vp + t * 4 + grp];
+          const uint32_t w = vpw[4 * ks + slot];
           const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xFFFF0000u);
           const float p = live ? ws.P[prow][t] : 0.f;
           const float z = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
           zacc[gi] = fmaf(p, z, zacc[gi]);
           x[slot] = p * (hi - lo) * vscale[2 * ks + khalf];
         }
-        split2(x[0], x[1], vb[gi][ks][0], vb[gi][ks][2]);
-        split2(x[2], x[3], vb[gi][ks][1], vb[gi][ks][3]);
+        vb[gi][ks][0] = pack_f16x2(x[0], x[1]);
+        vb[gi][ks][1] = pack_f16x2(x[2], x[3]);
       }
     }
     // value codes of this lane
     uint32_t vw[4 * BITS];
-    if (BITS == 2) {
+    {
       const uint4 w0 = *reinterpret_cast<const uint4*>(S + SL::vc + lane * 4);
-      const uint4 w1 = *reinterpret_cast<const uint4*>(S + SL::vc + 128 + lane * 4);
-      vw[0] = w0.x; vw[1] = w0.y; vw[2] = w0.z; vw[3] = w0.w;
-      vw[4 % (4 * BITS)] = w1.x; vw[5 % (4 * BITS)] = w1.y; vw[6 % (4 * BITS)] = w1.z; vw[7 % (4 * BITS)] = w1.w;
-    } else {
-      const uint4 w0 = *reinterpret_cast<const uint4*>(S + SL::vc + lane * 4);
-      vw[0] = w0.x; vw[1] = w0.y; vw[2] = w0.z; vw[3] = w0.w;
+      vw[0] = w0.x;
+      vw[1] = w0.y;
+      vw[2] = w0.z;
+      vw[3] = w0.w;
+      if (BITS == 2) {
+        const uint4 w1 = *reinterpret_cast<const uint4*>(S + SL::vc + 128 + lane * 4);
+        vw[4 % (4 * BITS)] = w1.x;
+        vw[5 % (4 * BITS)] = w1.y;
+        vw[6 % (4 * BITS)] = w1.z;
+        vw[7 % (4 * BITS)] = w1.w;
+      }
     }
     __syncwarp();
     // the stage is consumed: refill it with block it + kStages (async proxy after generic reads)
@@ -680,7 +732,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         }
         const int gi = PG ? 0 : (mt >> 1);
         mma16816(dv[mt], a0, a1, a2, a3, vb[gi][ks][0], vb[gi][ks][1]);
-        mma16816(dv[mt], a0, a1, a2, a3, vb[gi][ks][2], vb[gi][ks][3]);
       }
     }
     bm = nbm;
@@ -693,8 +744,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     for (int s = 0; s < kStages; ++s)
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&ws.bar[s])) : "memory");
   }
-  l_run[0] = warp_sum_g(l_run[0]);
-  l_run[1] = warp_sum_g(l_run[1]);
+#pragma unroll
+  for (int e = 0; e < RPL; ++e) l_run[e] = warp_sum_g(l_run[e]);
 #pragma unroll
   for (int i = 0; i < (PG ? 1 : 4); ++i) {  // z sums over the 4 lanes of a row group
     zacc[i] += __shfl_xor_sync(0xffffffffu, zacc[i], 1);
@@ -703,13 +754,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
   __syncthreads();
   MergeSmem<NR>& ms = *reinterpret_cast<MergeSmem<NR>*>(smem_raw);
   if (gq == 0) {
-    if (2 * tq < NR) {
-      ms.m[warp][2 * tq] = m_run[0];
-      ms.l[warp][2 * tq] = l_run[0];
-    }
-    if (2 * tq + 1 < NR) {
-      ms.m[warp][2 * tq + 1] = m_run[1];
-      ms.l[warp][2 * tq + 1] = l_run[1];
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) {
+      if (jr[e] < NR) {
+        ms.m[warp][jr[e]] = m_run[e];
+        ms.l[warp][jr[e]] = l_run[e];
+      }
     }
   }
   if (PG) {
@@ -751,8 +801,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     }
   }
   __syncthreads();
-  const int R = NR;
-  const size_t base = (((size_t)b * G.H + h) * (a.nsplit + 1) + split) * R;
+  const size_t base = (((size_t)b * G.H + h) * (a.nsplit + 1) + split) * NR;
   for (int i = threadIdx.x; i < NR * 128; i += kThreads) {
     const int j = i >> 7, c = i & 127;
     float M = -CUDART_INF_F;

@@ -189,6 +189,20 @@ __host__ __device__ inline void vloc(const Geo& G, int t, int c, int* word, int*
   }
 }
 
+// Group-param word index within a block.  Generic: key c -> c, value (t, j) ->
+// t*nch + j.  Fast layout: permuted so every lane of the MMA kernel reads its
+// own params with 128-bit loads: key channel c = 32*tk + ks + 8*m is owned by
+// lane 8*tk + ks (word 4*lane + m); value (token t, group j) sits at
+// 32*j + 8*tq + 4*ks + slot with t = 16*ks + 2*tq + (slot & 1) + 8*(slot >> 1).
+__host__ __device__ inline int kpi(const Geo& G, int c) {
+  return G.fast ? (8 * (c >> 5) + (c & 7)) * 4 + ((c >> 3) & 3) : c;
+}
+__host__ __device__ inline int vpi(const Geo& G, int t, int j) {
+  if (!G.fast) return t * G.nch + j;
+  const int ks = t >> 4, khalf = (t >> 3) & 1, tq = (t >> 1) & 3, odd = t & 1;
+  return 32 * j + 8 * tq + 4 * ks + 2 * khalf + odd;
+}
+
 __device__ inline uint32_t read_code(const uint32_t* blk_words, int word, int bit, int bits) {
   return (blk_words[word] >> bit) & ((1u << bits) - 1u);
 }

@@ -23,7 +23,7 @@ __device__ inline float dq_key(const Geo& G, const LayerBufs& B, size_t bi, int 
   int w, bit;
   kloc(G, t, c, &w, &bit);
   uint32_t code = read_code(B.kcodes + bi * (size_t)G.bwords, w, bit, G.bits);
-  return dequant_exact(code, params_from_word(B.kparams[bi * G.d + c], G.bits));
+  return dequant_exact(code, params_from_word(B.kparams[bi * G.d + kpi(G, c)], G.bits));
 }
 __device__ inline float dq_val(const Geo& G, const LayerBufs& B, size_t bi, int t, int c) {
   if (G.bits == 16)
@@ -32,7 +32,7 @@ __device__ inline float dq_val(const Geo& G, const LayerBufs& B, size_t bi, int 
   vloc(G, t, c, &w, &bit);
   uint32_t code = read_code(B.vcodes + bi * (size_t)G.bwords, w, bit, G.bits);
   return dequant_exact(code, params_from_word(
-      B.vparams[bi * (size_t)(G.g * G.nch) + t * G.nch + c / G.g], G.bits));
+      B.vparams[bi * (size_t)(G.g * G.nch) + vpi(G, t, c / G.g)], G.bits));
 }
 
 // One CTA (kCH threads, named barrier 1) of the exact path for (split, h, b).

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
       lo = fminf(lo, x);
       hi = fmaxf(hi, x);
     }
-    B.kparams[bi * d + c] = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+    B.kparams[bi * d + kpi(G, c)] = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
     atomicMax(reinterpret_cast<unsigned*>(&s_rk), __float_as_uint(hi - lo));
     GroupParams p = params_from_minmax((double)lo, (double)hi, G.bits);
     kz[c] = p.zero;
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
       lo = fminf(lo, x);
       hi = fmaxf(hi, x);
     }
-    B.vparams[bi * (size_t)(g * G.nch) + i] =
+    B.vparams[bi * (size_t)(g * G.nch) + vpi(G, t, j)] =
         float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
     atomicMax(reinterpret_cast<unsigned*>(&s_rv), __float_as_uint(hi - lo));
     GroupParams p = params_from_minmax((double)lo, (double)hi, G.bits);
@@ -161,7 +161,7 @@ __global__ void k_export(Geo G, LayerBufs B, int seq, int nblocks, uint8_t* kcod
     kcodes[(((size_t)blk * G.H + h) * d + c) * nb + byte] = (uint8_t)v;
   }
   for (int c = tid; c < d; c += blockDim.x) {
-    GroupParams p = params_from_word(B.kparams[bi * d + c], bits);
+    GroupParams p = params_from_word(B.kparams[bi * d + kpi(G, c)], bits);
     size_t o = ((size_t)blk * G.H + h) * d + c;
     kzero[o] = double_to_half_bits_rn(p.zero);
     kscale[o] = double_to_half_bits_rn(p.scale);
@@ -181,7 +181,7 @@ __global__ void k_export(Geo G, LayerBufs B, int seq, int nblocks, uint8_t* kcod
   }
   for (int i = tid; i < g * G.nch; i += blockDim.x) {
     int t = i / G.nch, j = i - t * G.nch;
-    GroupParams p = params_from_word(B.vparams[bi * (size_t)(g * G.nch) + i], bits);
+    GroupParams p = params_from_word(B.vparams[bi * (size_t)(g * G.nch) + vpi(G, t, j)], bits);
     size_t o = (((size_t)blk * g + t) * G.H + h) * G.nch + j;
     vzero[o] = double_to_half_bits_rn(p.zero);
     vscale[o] = double_to_half_bits_rn(p.scale);
@@ -206,7 +206,7 @@ __device__ inline float packed_key(const Geo& G, const LayerBufs& B, int b, int 
   int w, bit;
   kloc(G, t, c, &w, &bit);
   uint32_t code = read_code(B.kcodes + bi * (size_t)G.bwords, w, bit, G.bits);
-  return dequant_exact(code, params_from_word(B.kparams[bi * G.d + c], G.bits));
+  return dequant_exact(code, params_from_word(B.kparams[bi * G.d + kpi(G, c)], G.bits));
 }
 __device__ inline float packed_val(const Geo& G, const LayerBufs& B, int b, int h, int pos, int c) {
   int blk = pos / G.g, t = pos - blk * G.g;
@@ -216,7 +216,7 @@ __device__ inline float packed_val(const Geo& G, const LayerBufs& B, int b, int 
   int w, bit;
   vloc(G, t, c, &w, &bit);
   uint32_t code = read_code(B.vcodes + bi * (size_t)G.bwords, w, bit, G.bits);
-  return dequant_exact(code, params_from_word(B.vparams[bi * (size_t)(G.g * G.nch) + t * G.nch + c / G.g], G.bits));
+  return dequant_exact(code, params_from_word(B.vparams[bi * (size_t)(G.g * G.nch) + vpi(G, t, c / G.g)], G.bits));
 }
 
 __global__ void k_materialize(Geo G, LayerBufs B, int b, int h, int n, int f, float* keys,
