@@ -650,12 +650,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     }
     __syncwarp();
 
-    // ---- value B fragments (single f16 plane) -------------------------------------------
+    // ---- value B fragments (f16 hi + lo: sum_t P*z and sum_t P*s*code may nearly cancel)
     // PG: lane column n = gq -> (grp = gq / NR, row = gq % NR); else row = gq, per group
-    uint32_t vb[PG ? 1 : 4][2][2];  // [grp][ks] {b0, b1}
+    uint32_t vb[PG ? 1 : 4][2][4];  // [grp][ks] {b0hi, b1hi, b0lo, b1lo}
 #pragma unroll
     for (int gi = 0; gi < (PG ? 1 : 4); ++gi) {
-      const int grp = PG ? (gq / NR) : gi;
+      const int grp = PG ? ((gq / NR) & 3) : gi;
       const int row = PG ? (gq % NR) : gq;
       const bool live = PG ? (gq < 4 * NR) : (gq < NR);
       const int prow = row < NR ? row : 0;
@@ -676,8 +676,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
           zacc[gi] = fmaf(p, z, zacc[gi]);
           x[slot] = p * (hi - lo) * vscale[2 * ks + khalf];
         }
-        vb[gi][ks][0] = pack_f16x2(x[0], x[1]);
-        vb[gi][ks][1] = pack_f16x2(x[2], x[3]);
+        split2(x[0], x[1], vb[gi][ks][0], vb[gi][ks][2]);
+        split2(x[2], x[3], vb[gi][ks][1], vb[gi][ks][3]);
       }
     }
     // value codes of this lane
@@ -732,6 +732,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         }
         const int gi = PG ? 0 : (mt >> 1);
         mma16816(dv[mt], a0, a1, a2, a3, vb[gi][ks][0], vb[gi][ks][1]);
+        mma16816(dv[mt], a0, a1, a2, a3, vb[gi][ks][2], vb[gi][ks][3]);
       }
     }
     bm = nbm;

@@ -25,8 +25,18 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--impl", default="auto")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--ctx", type=int, default=0)
+    ap.add_argument("--heads", type=int, default=0)
     args = ap.parse_args()
     cfg = dict(bench.CONFIGS[args.config])
+    if args.batch:
+        cfg["batch"] = args.batch
+    if args.ctx:
+        cfg["ctx"] = args.ctx
+    if args.heads:
+        g = cfg["q_heads"] // cfg["kv_heads"]
+        cfg["kv_heads"], cfg["q_heads"] = args.heads, args.heads * g
     cfg["layers"] = 1
     dev = "cuda:0"
     budget = CacheBudget(bits=cfg["bits"], group_size=cfg["group"], residual=cfg["residual"],
