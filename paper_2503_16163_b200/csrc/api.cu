@@ -2,13 +2,16 @@
 // per-layer ticket protocol, and the K1..K6 launch sequence of one decode layer.
 //
 // Stream structure per layer l (SURVEY.md 8(b) "Threading"):
-//   compute stream : [wait ev_pf(l)] K2 attend -> K3 combine -> K3 agg
-//                    -> record ev_agg(l) -> K6 append (+K1 migration)
-//   copy stream    : [wait ev_agg(l)] K4 top-k + pin diff -> K5 prefetch
-//                    -> record ev_pf(l)
-// so the selection and the PCIe gather for step t+1 overlap the compute of the
-// following layers; decode_layer(l, t+1) waits on ev_pf(l) -- the device form
-// of SimulatedChannel.await_layer (transfer.py:96-100).
+//   compute stream     : [wait ev_pf(l)] K2 attend (+K3 combine) -> K6a ring
+//                        append -> record ev_att(l)
+//   copy stream l % 2  : [wait ev_att(l)] K3 cross-head aggregate -> K4 top-k +
+//   (high priority)      pin diff -> K5 PCIe prefetch -> K6b slow-tier write
+//                        (+K1 migration) -> record ev_pf(l)
+// Only attention sits on the caller's stream; the selection, the PCIe gather
+// and the slow-tier write for step t+1 overlap the next layers' attention.
+// decode_layer(l, t+1) waits on ev_pf(l) -- the device form of
+// SimulatedChannel.await_layer (transfer.py:96-100).  Spill buffers are per
+// layer so the aggregate can lag the compute stream.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -55,8 +58,9 @@ struct spc_cache {
   size_t host_bytes = 0, dev_bytes = 0, slab_elems = 0;
   std::vector<int64_t> n, f;
   std::vector<int> ticket;  // pending ticket step per layer (-1 none)
-  cudaStream_t copy_stream = nullptr;
+  cudaStream_t copy_stream = nullptr, copy_stream2 = nullptr;
   std::vector<cudaEvent_t> ev_agg, ev_pf;
+  cudaStream_t cstream(int layer) const { return (layer & 1) ? copy_stream2 : copy_stream; }
   float *part_o = nullptr, *part_ml = nullptr, *pin_ml = nullptr, *spill = nullptr, *mz = nullptr;
   int32_t* staging = nullptr;
   int context_length = 0;
@@ -115,18 +119,20 @@ int migrate(spc_cache* c, int layer, cudaStream_t st) {
   return SPC_OK;
 }
 
+// append_verified on one stream: ring + slow tier + migration (kvcache.py:162-171)
 int append_rows(spc_cache* c, int layer, const void* kr, const void* vr, int64_t seq_stride,
                 cudaStream_t st) {
   const Geo& G = c->G;
   if (c->n[layer] >= c->context_length)
     return fail(SPC_EINVAL, "context_length exceeded");
-  c->launches += 1;
-  launch_append(G, c->L[layer], (const __nv_bfloat16*)kr, (const __nv_bfloat16*)vr,
-                seq_stride ? seq_stride : (int64_t)G.H * G.d, (int)c->n[layer],
-                host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer), st);
+  launch_ring_append(G, c->L[layer], (const __nv_bfloat16*)kr, (const __nv_bfloat16*)vr,
+                     seq_stride ? seq_stride : (int64_t)G.H * G.d, (int)c->n[layer], st);
+  launch_host_append(G, c->L[layer], (int)c->n[layer], host_slab(c, c->host_k, layer),
+                     host_slab(c, c->host_v, layer), st);
+  c->launches += 2;
   CUDA_TRY(cudaGetLastError());
   c->n[layer] += 1;
-  while (c->n[layer] - c->f[layer] >= G.r + G.g) {  // kvcache.py:169-171
+  while (c->n[layer] - c->f[layer] >= G.r + G.g) {
     int rc = migrate(c, layer, st);
     if (rc) return rc;
   }
@@ -142,9 +148,12 @@ cudaEvent_t prof_event(spc_cache* c) {
   return c->ev_pool[c->ev_used++];
 }
 
+// One decode / predecode layer.  append_row0: decode persists row 0 (engine.py:321).
 int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_new,
-              const void* v_new, void* out, float* pinned_mass, cudaStream_t st) {
+              const void* v_new, void* out, float* pinned_mass, cudaStream_t st, bool append_row0) {
   const Geo& G = c->G;
+  if (append_row0 && c->n[layer] >= c->context_length)
+    return fail(SPC_EINVAL, "context_length exceeded");
   AttnArgs a{};
   a.G = G;
   a.B = c->L[layer];
@@ -160,8 +169,8 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
   a.part_o = c->part_o;
   a.part_ml = c->part_ml;
   a.pin_ml = c->pin_ml;
-  a.spill = c->spill;
-  a.mz = c->mz;
+  a.spill = c->spill + (size_t)layer * G.batch * G.Hq * (size_t)G.L;
+  a.mz = c->mz + (size_t)layer * G.batch * G.Hq * 2;
   a.sm_scale_log2 = (float)(1.0 / std::sqrt((double)G.d) * 1.4426950408889634);
   bool fast = (c->impl != 1) && attend_fast_supported(G, rows);
   if (c->impl == 2 && !fast) return fail(SPC_EINVAL, "fast attention path not available for this geometry");
@@ -172,7 +181,7 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
     CUDA_TRY(cudaEventRecord(p0, st));
   }
   if (fast) {
-    c->launches += launch_attend_fast(a, st);  // K2 (+ fused combine); own split plan
+    c->launches += launch_attend_fast(a, st);  // K2 + K3 combine; own split plan
   } else {
     choose_splits(c, a.f, &a.nsplit, &a.blocks_per_split);
     launch_attend_generic(a, st);
@@ -185,28 +194,44 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
     CUDA_TRY(cudaEventRecord(p1, st));
     c->prof_attn.push_back({p0, p1});
   }
-  launch_agg(a, st);
-  c->launches += a.f > 0;
-  CUDA_TRY(cudaGetLastError());
-  // ticket: selection + prefetch on the copy stream (transfer.py:84-94)
+  const int n_before = (int)c->n[layer];
+  if (append_row0) {  // K6a on the compute stream (reads the caller's k_new/v_new now)
+    launch_ring_append(G, c->L[layer], (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new,
+                       (long long)rows * G.H * G.d, n_before, st);
+    c->launches += 1;
+    CUDA_TRY(cudaGetLastError());
+  }
   CUDA_TRY(cudaEventRecord(c->ev_agg[layer], st));
-  CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev_agg[layer], 0));
+  // ---- ticket + slow tier on a copy stream (transfer.py:84-94, kvcache.py:162-192) ----
+  cudaStream_t cs = c->cstream(layer);
+  CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_agg[layer], 0));
   if (c->prof) {
     p0 = prof_event(c);
     p1 = prof_event(c);
-    CUDA_TRY(cudaEventRecord(p0, c->copy_stream));
+    CUDA_TRY(cudaEventRecord(p0, cs));
   }
-  launch_topk(G, c->L[layer], a.f, c->copy_stream);
-  CUDA_TRY(cudaGetLastError());
-  launch_prefetch(G, c->L[layer], host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer),
-                  c->copy_stream);
+  launch_agg(a, cs);
+  c->launches += a.f > 0;
+  launch_topk(G, c->L[layer], a.f, cs);
+  launch_prefetch(G, c->L[layer], host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer), cs);
   c->launches += 2;
   CUDA_TRY(cudaGetLastError());
   if (c->prof) {
-    CUDA_TRY(cudaEventRecord(p1, c->copy_stream));
+    CUDA_TRY(cudaEventRecord(p1, cs));
     c->prof_sel.push_back({p0, p1});
   }
-  CUDA_TRY(cudaEventRecord(c->ev_pf[layer], c->copy_stream));
+  if (append_row0) {
+    launch_host_append(G, c->L[layer], n_before, host_slab(c, c->host_k, layer),
+                       host_slab(c, c->host_v, layer), cs);
+    c->launches += 1;
+    c->n[layer] += 1;
+    while (c->n[layer] - c->f[layer] >= G.r + G.g) {  // kvcache.py:169-171
+      int rc = migrate(c, layer, cs);
+      if (rc) return rc;
+    }
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaEventRecord(c->ev_pf[layer], cs));
   return SPC_OK;
 }
 }  // namespace
@@ -313,8 +338,8 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
   if (rc == SPC_OK) rc = dalloc(c, (void**)&c->part_o, b * H * (kSplitCap + 1) * R * G.d * 4);
   if (rc == SPC_OK) rc = dalloc(c, (void**)&c->part_ml, b * H * (kSplitCap + 1) * R * 2 * 4);
   if (rc == SPC_OK) rc = dalloc(c, (void**)&c->pin_ml, b * H * R * 2 * 4);
-  if (rc == SPC_OK) rc = dalloc(c, (void**)&c->spill, b * G.Hq * (size_t)G.L * 4);
-  if (rc == SPC_OK) rc = dalloc(c, (void**)&c->mz, b * G.Hq * 2 * 4);
+  if (rc == SPC_OK) rc = dalloc(c, (void**)&c->spill, (size_t)G.layers * b * G.Hq * (size_t)G.L * 4);
+  if (rc == SPC_OK) rc = dalloc(c, (void**)&c->mz, (size_t)G.layers * b * G.Hq * 2 * 4);
   if (rc == SPC_OK) rc = dalloc(c, (void**)&c->staging, (size_t)G.k * 4);
   if (rc == SPC_OK) {
     c->slab_elems = b * (size_t)G.L * H * G.d;
@@ -328,7 +353,10 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
                                 " bytes): " + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
   }
   if (rc == SPC_OK) {
-    if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    if (cudaStreamCreateWithPriority(&c->copy_stream, cudaStreamNonBlocking, hi_prio) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->copy_stream2, cudaStreamNonBlocking, hi_prio) != cudaSuccess)
       rc = fail(SPC_ECUDA, "stream create failed");
     c->ev_agg.resize(G.layers);
     c->ev_pf.resize(G.layers);
@@ -363,6 +391,7 @@ int spc_cache_destroy(spc_cache* c) {
   for (auto e : c->ev_agg) if (e) cudaEventDestroy(e);
   for (auto e : c->ev_pf) if (e) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->copy_stream2) cudaStreamDestroy(c->copy_stream2);
   delete c;
   return SPC_OK;
 }
@@ -413,6 +442,7 @@ int spc_append(spc_cache* c, int layer, const void* k_rows, const void* v_rows, 
                void* stream) {
   if (int rc = check_layer(c, layer)) return rc;
   CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_pf[layer], 0));
   return append_rows(c, layer, k_rows, v_rows, seq_stride, (cudaStream_t)stream);
 }
 
@@ -473,7 +503,7 @@ int spc_predecode_layer(spc_cache* c, int layer, const void* q, const void* k_ne
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));
-  int rc = run_layer(c, layer, 1, q, k_new, v_new, out, nullptr, st);
+  int rc = run_layer(c, layer, 1, q, k_new, v_new, out, nullptr, st, false);
   if (rc) return rc;
   c->ticket[layer] = 0;
   return SPC_OK;
@@ -489,11 +519,11 @@ int spc_decode_layer(spc_cache* c, int layer, int step, const void* q, const voi
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));  // await_layer
   c->ticket[layer] = -1;
-  int rc = run_layer(c, layer, 2, q, k_new, v_new, out, pinned_mass, st);
+  // persists row 0 only (engine.py:321; the speculative row is never persisted)
+  int rc = run_layer(c, layer, 2, q, k_new, v_new, out, pinned_mass, st, true);
   if (rc) return rc;
   c->ticket[layer] = step;
-  // persist row 0 only (engine.py:321; SPEC: the speculative row is never persisted)
-  return append_rows(c, layer, k_new, v_new, (int64_t)2 * c->G.H * c->G.d, st);
+  return SPC_OK;
 }
 
 int spc_ticket(spc_cache* c, int layer, int32_t* picked, int32_t* new_count, void* stream) {

@@ -20,6 +20,8 @@
 // in the log2 domain; K3 merges them.
 #include <math_constants.h>
 
+#include <algorithm>
+
 #include "exact_segment.cuh"
 
 namespace spc {
@@ -92,24 +94,28 @@ void launch_combine(const AttnArgs& a, cudaStream_t st) {
 
 // K3b: agg[i] = sum over the unit's q heads of A_j[agg_row, i], i < f, in
 // ascending head order like np.sum(axis=0) (engine.py:317).
-__global__ void k_agg(AttnArgs a) {
+__global__ void __launch_bounds__(256) k_agg(AttnArgs a) {
   const Geo G = a.G;
   const int u = blockIdx.y, b = blockIdx.z;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.f) return;
   const int h0 = G.scope ? u * G.G : 0, h1 = G.scope ? (u + 1) * G.G : G.Hq;
-  float acc = 0.f;
-  for (int hq = h0; hq < h1; ++hq) {
-    float M = a.mz[((size_t)b * G.Hq + hq) * 2], L = a.mz[((size_t)b * G.Hq + hq) * 2 + 1];
-    float p = exp2f(a.spill[((size_t)b * G.Hq + hq) * G.L + i] - M) / L;
-    acc += p;
+  __shared__ float sM[256], sI[256];
+  for (int x = threadIdx.x; x < h1 - h0; x += blockDim.x) {
+    sM[x] = a.mz[((size_t)b * G.Hq + h0 + x) * 2];
+    sI[x] = 1.f / a.mz[((size_t)b * G.Hq + h0 + x) * 2 + 1];
   }
-  a.B.agg[((size_t)b * G.U + u) * G.L + i] = acc;
+  __syncthreads();
+  const float* sp = a.spill + ((size_t)b * G.Hq + h0) * G.L;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.f; i += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int x = 0; x < h1 - h0; ++x) acc += exp2f(sp[(size_t)x * G.L + i] - sM[x]) * sI[x];
+    a.B.agg[((size_t)b * G.U + u) * G.L + i] = acc;
+  }
 }
 
 void launch_agg(const AttnArgs& a, cudaStream_t st) {
   if (a.f <= 0) return;
-  k_agg<<<dim3((a.f + 255) / 256, a.G.U, a.G.batch), 256, 0, st>>>(a);
+  const int blocks = std::min((a.f + 255) / 256, std::max(1, 2 * 148 * 4 / (a.G.U * a.G.batch)));
+  k_agg<<<dim3(blocks, a.G.U, a.G.batch), 256, 0, st>>>(a);
 }
 
 }  // namespace spc

@@ -62,9 +62,10 @@ void launch_prefetch_one(const Geo& G, const LayerBufs& B, int seq, int unit,
                          const __nv_bfloat16* host_k, const __nv_bfloat16* host_v, cudaStream_t st);
 void launch_copy_pins(const Geo& G, const LayerBufs& B, int seq, int unit, const __nv_bfloat16* k_rows,
                       const __nv_bfloat16* v_rows, int npos, cudaStream_t st);
-void launch_append(const Geo& G, const LayerBufs& B, const __nv_bfloat16* k_rows,
-                   const __nv_bfloat16* v_rows, long long seq_stride, int n,
-                   __nv_bfloat16* host_k, __nv_bfloat16* host_v, cudaStream_t st);
+void launch_ring_append(const Geo& G, const LayerBufs& B, const __nv_bfloat16* k_rows,
+                        const __nv_bfloat16* v_rows, long long seq_stride, int n, cudaStream_t st);
+void launch_host_append(const Geo& G, const LayerBufs& B, int n, __nv_bfloat16* host_k,
+                        __nv_bfloat16* host_v, cudaStream_t st);
 void launch_ring_fill(const Geo& G, const LayerBufs& B, const __nv_bfloat16* K,
                       const __nv_bfloat16* V, int n, int f, cudaStream_t st);
 

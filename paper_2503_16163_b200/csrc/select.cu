@@ -303,27 +303,42 @@ void launch_copy_pins(const Geo& G, const LayerBufs& B, int seq, int unit, const
   if (npos > 0) k_copy_pins<<<npos, 256, 0, st>>>(G, B, seq, unit, k_rows, v_rows);
 }
 
-// K6: append row 0 at position n: residual ring slot n % (r+g) and slow tier.
-__global__ void k_append(Geo G, LayerBufs B, const __nv_bfloat16* kr, const __nv_bfloat16* vr,
-                         long long seq_stride, int n, __nv_bfloat16* host_k, __nv_bfloat16* host_v) {
+// K6a: append row 0 at position n to the residual ring (compute stream; the
+// ring slot n % (r+g) is not read by this step's attention).
+__global__ void k_ring_append(Geo G, LayerBufs B, const __nv_bfloat16* kr, const __nv_bfloat16* vr,
+                              long long seq_stride, int n) {
   const int b = blockIdx.x;
   const int slot = n % G.ring;
   for (int x = threadIdx.x; x < G.H * G.d; x += blockDim.x) {
-    int h = x / G.d, c = x - h * G.d;
-    __nv_bfloat16 kv = kr[(size_t)b * seq_stride + x], vv = vr[(size_t)b * seq_stride + x];
-    size_t ro = (((size_t)b * G.H + h) * G.ring + slot) * G.d + c;
-    B.ring_k[ro] = kv;
-    B.ring_v[ro] = vv;
-    size_t ho = (((size_t)b * G.L + n) * G.H + h) * G.d + c;
-    host_k[ho] = kv;
-    host_v[ho] = vv;
+    const int h = x / G.d, c = x - h * G.d;
+    const size_t ro = (((size_t)b * G.H + h) * G.ring + slot) * G.d + c;
+    B.ring_k[ro] = kr[(size_t)b * seq_stride + x];
+    B.ring_v[ro] = vr[(size_t)b * seq_stride + x];
   }
 }
 
-void launch_append(const Geo& G, const LayerBufs& B, const __nv_bfloat16* k_rows,
-                   const __nv_bfloat16* v_rows, long long seq_stride, int n,
-                   __nv_bfloat16* host_k, __nv_bfloat16* host_v, cudaStream_t st) {
-  k_append<<<G.batch, 256, 0, st>>>(G, B, k_rows, v_rows, seq_stride, n, host_k, host_v);
+// K6b: persist the row to the slow tier (pinned host, zero-copy store) from its
+// ring slot (copy stream).
+__global__ void k_host_append(Geo G, LayerBufs B, int n, __nv_bfloat16* host_k, __nv_bfloat16* host_v) {
+  const int b = blockIdx.x;
+  const int slot = n % G.ring;
+  for (int x = threadIdx.x; x < G.H * G.d; x += blockDim.x) {
+    const int h = x / G.d, c = x - h * G.d;
+    const size_t ro = (((size_t)b * G.H + h) * G.ring + slot) * G.d + c;
+    const size_t ho = (((size_t)b * G.L + n) * G.H + h) * G.d + c;
+    host_k[ho] = B.ring_k[ro];
+    host_v[ho] = B.ring_v[ro];
+  }
+}
+
+void launch_ring_append(const Geo& G, const LayerBufs& B, const __nv_bfloat16* k_rows,
+                        const __nv_bfloat16* v_rows, long long seq_stride, int n, cudaStream_t st) {
+  k_ring_append<<<G.batch, 256, 0, st>>>(G, B, k_rows, v_rows, seq_stride, n);
+}
+
+void launch_host_append(const Geo& G, const LayerBufs& B, int n, __nv_bfloat16* host_k,
+                        __nv_bfloat16* host_v, cudaStream_t st) {
+  k_host_append<<<G.batch, 256, 0, st>>>(G, B, n, host_k, host_v);
 }
 
 // Prefill: residual rows [f, n) of K/V [b][n][H][d] into the ring.
