@@ -289,15 +289,15 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
   G.vrw = G.krw;
   G.fast = (G.d == 128 && G.g == 32 && (G.bits == 1 || G.bits == 2)) ? 1 : 0;
   G.bwords = G.g * G.krw;
+  G.rec = 2 * G.bwords + (G.bits == 16 ? 0 : G.d + G.g * G.nch);
 
   int rc = SPC_OK;
   const size_t b = G.batch, H = G.H, U = G.U;
   c->L.resize(G.layers);
   for (int l = 0; l < G.layers && rc == SPC_OK; ++l) {
     LayerBufs& B = c->L[l];
-    size_t codes = b * H * G.nblk * (size_t)G.bwords * 4;
-    size_t kpar = G.bits == 16 ? 0 : b * H * G.nblk * (size_t)G.d * 4;
-    size_t vpar = G.bits == 16 ? 0 : b * H * G.nblk * (size_t)G.g * G.nch * 4;
+    size_t codes = b * H * G.nblk * (size_t)G.rec * 4;  // block records
+    size_t kpar = 0, vpar = 0;
     size_t ring = b * H * G.ring * (size_t)G.d * 2;
     size_t pool = b * U * G.k * (size_t)G.Hu * G.d * 2;
     size_t off[16], tot = 0, sizes[16] = {codes, codes, kpar, vpar, ring, ring, pool, pool,
@@ -312,9 +312,9 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
     rc = dalloc(c, (void**)&base, tot);
     if (rc) break;
     B.kcodes = (uint32_t*)(base + off[0]);
-    B.vcodes = (uint32_t*)(base + off[1]);
-    B.kparams = (uint32_t*)(base + off[2]);
-    B.vparams = (uint32_t*)(base + off[3]);
+    B.vcodes = B.kcodes + G.bwords;
+    B.kparams = B.kcodes + 2 * G.bwords;
+    B.vparams = B.kparams + (G.bits == 16 ? 0 : G.d);
     B.ring_k = (__nv_bfloat16*)(base + off[4]);
     B.ring_v = (__nv_bfloat16*)(base + off[5]);
     B.pool_k = (__nv_bfloat16*)(base + off[6]);

@@ -72,6 +72,12 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
   lo = pack_f16x2(x0 - hf.x, x1 - hf.y);
 }
 
+__device__ __forceinline__ float fast_exp2(float x) {  // ex2.approx (|rel err| ~2^-22); -inf -> 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float pow2i(int e) {  // 2^e, e in [-126, 127]
   return __int_as_float((127 + e) << 23);
 }
@@ -276,7 +282,7 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
       const float mold = ex.m[j], mnew = fmaxf(mold, mx);
       float sum = 0.f;
       for (int i = lane; i < count; i += 32) {
-        const float p = mnew == -CUDART_INF_F ? 0.f : exp2f(ex.sc[j][i] - mnew);
+        const float p = mnew == -CUDART_INF_F ? 0.f : fast_exp2(ex.sc[j][i] - mnew);
         ex.sc[j][i] = p;
         sum += p;
       }
@@ -371,20 +377,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
   const int blk1 = min(nb_total, blk0 + a.blocks_per_split);
   const float cs = BITS == 1 ? 0.5f : (1.f / 3.f);
   const size_t bi0 = blk_index(G, b, h, 0);
-  const uint32_t* kc_base = B.kcodes + bi0 * (size_t)G.bwords;
-  const uint32_t* vc_base = B.vcodes + bi0 * (size_t)G.bwords;
-  const uint32_t* kp_base = B.kparams + bi0 * 128;
-  const uint32_t* vp_base = B.vparams + bi0 * 128;
+  const uint32_t* rec_base = B.kcodes + bi0 * (size_t)SL::words;
   const uint32_t* bm_base = B.bitmap + ((size_t)b * G.U + (G.scope ? h : 0)) * (G.L / 32);
 
   // ---- TMA ring prologue -------------------------------------------------------------
   auto issue = [&](int blk, int st) {
     uint32_t* s = ws.stage[st];
-    mbar_expect_tx(&ws.bar[st], SL::bytes);
-    tma_load(s + SL::kc, kc_base + (size_t)blk * G.bwords, SL::code_bytes, &ws.bar[st]);
-    tma_load(s + SL::vc, vc_base + (size_t)blk * G.bwords, SL::code_bytes, &ws.bar[st]);
-    tma_load(s + SL::kp, kp_base + (size_t)blk * 128, 512, &ws.bar[st]);
-    tma_load(s + SL::vp, vp_base + (size_t)blk * 128, 512, &ws.bar[st]);
+    mbar_expect_tx(&ws.bar[st], SL::bytes);  // the whole block record, one bulk copy
+    tma_load(s, rec_base + (size_t)blk * SL::words, SL::bytes, &ws.bar[st]);
   };
   if (lane == 0) {
 #pragma unroll
@@ -463,13 +463,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     return (j & 1) ? x1 : x0;
   };
 
-  int it = 0;
+  int st = 0;
+  unsigned phase = 0;
   uint32_t bm = 0;
   if (blk0 + warp < blk1) bm = bm_base[blk0 + warp];
-  for (int blk = blk0 + warp; blk < blk1; blk += kWarps, ++it) {
-    const int st = it % kStages;
+  for (int blk = blk0 + warp; blk < blk1; blk += kWarps) {
     const uint32_t nbm = (blk + kWarps < blk1) ? bm_base[blk + kWarps] : 0u;
-    mbar_wait(&ws.bar[st], (it / kStages) & 1);
+    mbar_wait(&ws.bar[st], phase);
     const uint32_t* S = ws.stage[st];
 
     // ---- key B fragments (cooperative) + zero-point constants C_j -----------------------
@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
       float al[RPL];
 #pragma unroll
       for (int e = 0; e < RPL; ++e) {
-        al[e] = m_run[e] == -CUDART_INF_F ? 0.f : exp2f(m_run[e] - mn[e]);
+        al[e] = m_run[e] == -CUDART_INF_F ? 0.f : fast_exp2(m_run[e] - mn[e]);
         l_run[e] *= al[e];
         m_run[e] = mn[e];
       }
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         const int T = 16 * mt + gq + 8 * hf;
 #pragma unroll
         for (int e = 0; e < RPL; ++e) {
-          const float p = exp2f(sc[mt][hf][e] - m_run[e]);
+          const float p = fast_exp2(sc[mt][hf][e] - m_run[e]);
           l_run[e] += p;
           if (jr[e] < NR) ws.P[jr[e]][T] = p;
         }
@@ -736,6 +736,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
       }
     }
     bm = nbm;
+    if (++st == kStages) {
+      st = 0;
+      phase ^= 1u;
+    }
   }
 
   // ---- warp results -> shared, CTA merge -> partial ----------------------------------

@@ -1,16 +1,18 @@
 // common.cuh -- geometry, HBM layout and exact-arithmetic helpers shared by
 // every kernel of the SpeCache decode path (sm_100a).
 //
-// HBM layout per (layer) -- all arrays are [seq][kv head][...] so one
-// (seq, head) streams contiguous memory:
-//   kcodes  uint32 [b][H][nblk][g][krw]   key codes, token-major rows, LSB-first
+// HBM layout per (layer) -- blocks are [seq][kv head][block] records of G.rec
+// words, one contiguous record per g-token block so a block moves with a single
+// bulk copy; within a record (pointers kcodes/vcodes/kparams/vparams are the
+// field bases, the block stride is G.rec for all four):
+//   kcodes  uint32 [g][krw]               key codes, token-major rows, LSB-first
 //                                         channel order (the reference's key
 //                                         group is a column of this block)
-//   vcodes  uint32 [b][H][nblk][g*vrw]    value codes; token-major rows in the
+//   vcodes  uint32 [g*vrw]                value codes; token-major rows in the
 //                                         generic layout, MMA-fragment-native in
 //                                         the fast layout (see vloc)
-//   kparams uint32 [b][H][nblk][d]        bf16 (lo | hi<<16) per key group
-//   vparams uint32 [b][H][nblk][g][nch]   bf16 (lo | hi<<16) per value group
+//   kparams uint32 [d]                    bf16 (lo | hi<<16) per key group (kpi)
+//   vparams uint32 [g*nch]                bf16 (lo | hi<<16) per value group (vpi)
 //   ring_k/v bf16  [b][H][r+g][d]         residual window, slot = pos % (r+g)
 //   pool_k/v bf16  [b][U][k][Hu][d]       pinned full-precision rows (slots)
 //   pin_pos int32  [b][U][k]              position held by each slot (-1 empty)
@@ -41,6 +43,7 @@ struct Geo {
   int vrw;    // uint32 words per value-code row (generic) / per block = g*vrw
   int fast;   // fast MMA layout (d=128, g=32, bits 1|2)
   int bwords; // uint32 words of (key or value) codes per block = g*krw
+  int rec;    // uint32 words per block record [kcodes | vcodes | kparams | vparams]
 };
 
 struct LayerBufs {

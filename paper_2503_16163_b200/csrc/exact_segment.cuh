@@ -19,20 +19,20 @@ constexpr int kMaxD = 256;
 
 __device__ inline float dq_key(const Geo& G, const LayerBufs& B, size_t bi, int t, int c) {
   if (G.bits == 16)
-    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B.kcodes)[(bi * G.g + t) * G.d + c]);
+    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B.kcodes + bi * (size_t)G.rec)[t * G.d + c]);
   int w, bit;
   kloc(G, t, c, &w, &bit);
-  uint32_t code = read_code(B.kcodes + bi * (size_t)G.bwords, w, bit, G.bits);
-  return dequant_exact(code, params_from_word(B.kparams[bi * G.d + kpi(G, c)], G.bits));
+  uint32_t code = read_code(B.kcodes + bi * (size_t)G.rec, w, bit, G.bits);
+  return dequant_exact(code, params_from_word(B.kparams[bi * G.rec + kpi(G, c)], G.bits));
 }
 __device__ inline float dq_val(const Geo& G, const LayerBufs& B, size_t bi, int t, int c) {
   if (G.bits == 16)
-    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B.vcodes)[(bi * G.g + t) * G.d + c]);
+    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B.vcodes + bi * (size_t)G.rec)[t * G.d + c]);
   int w, bit;
   vloc(G, t, c, &w, &bit);
-  uint32_t code = read_code(B.vcodes + bi * (size_t)G.bwords, w, bit, G.bits);
+  uint32_t code = read_code(B.vcodes + bi * (size_t)G.rec, w, bit, G.bits);
   return dequant_exact(code, params_from_word(
-      B.vparams[bi * (size_t)(G.g * G.nch) + vpi(G, t, c / G.g)], G.bits));
+      B.vparams[bi * (size_t)G.rec + vpi(G, t, c / G.g)], G.bits));
 }
 
 // One CTA (kCH threads, named barrier 1) of the exact path for (split, h, b).

@@ -39,8 +39,8 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
   const size_t bi = blk_index(G, b, h, blk);
 
   if (G.bits == 16) {  // verbatim full-precision tier (kvcache.py:185-187)
-    __nv_bfloat16* okc = reinterpret_cast<__nv_bfloat16*>(B.kcodes) + bi * (size_t)g * d;
-    __nv_bfloat16* ovc = reinterpret_cast<__nv_bfloat16*>(B.vcodes) + bi * (size_t)g * d;
+    __nv_bfloat16* okc = reinterpret_cast<__nv_bfloat16*>(B.kcodes + bi * (size_t)G.rec);
+    __nv_bfloat16* ovc = reinterpret_cast<__nv_bfloat16*>(B.vcodes + bi * (size_t)G.rec);
     for (int i = tid; i < g * d; i += nt) {
       okc[i] = __float2bfloat16_rn(sk[i]);
       ovc[i] = __float2bfloat16_rn(sv[i]);
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
       lo = fminf(lo, x);
       hi = fmaxf(hi, x);
     }
-    B.kparams[bi * d + kpi(G, c)] = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+    B.kparams[bi * G.rec + kpi(G, c)] = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
     atomicMax(reinterpret_cast<unsigned*>(&s_rk), __float_as_uint(hi - lo));
     GroupParams p = params_from_minmax((double)lo, (double)hi, G.bits);
     kz[c] = p.zero;
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
       lo = fminf(lo, x);
       hi = fmaxf(hi, x);
     }
-    B.vparams[bi * (size_t)(g * G.nch) + vpi(G, t, j)] =
+    B.vparams[bi * (size_t)G.rec + vpi(G, t, j)] =
         float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
     atomicMax(reinterpret_cast<unsigned*>(&s_rv), __float_as_uint(hi - lo));
     GroupParams p = params_from_minmax((double)lo, (double)hi, G.bits);
@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
     if (cv) atomicOr(&wv[w], cv << bit);
   }
   __syncthreads();
-  uint32_t* okc = B.kcodes + bi * (size_t)G.bwords;
-  uint32_t* ovc = B.vcodes + bi * (size_t)G.bwords;
+  uint32_t* okc = B.kcodes + bi * (size_t)G.rec;
+  uint32_t* ovc = B.vcodes + bi * (size_t)G.rec;
   for (int i = tid; i < G.bwords; i += nt) {
     okc[i] = wk[i];
     ovc[i] = wv[i];
@@ -144,8 +144,8 @@ __global__ void k_export(Geo G, LayerBufs B, int seq, int nblocks, uint8_t* kcod
   const int blk = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
   const int g = G.g, d = G.d, bits = G.bits, nb = (g * bits + 7) / 8;
   const size_t bi = blk_index(G, seq, h, blk);
-  const uint32_t* kw = B.kcodes + bi * (size_t)G.bwords;
-  const uint32_t* vw = B.vcodes + bi * (size_t)G.bwords;
+  const uint32_t* kw = B.kcodes + bi * (size_t)G.rec;
+  const uint32_t* vw = B.vcodes + bi * (size_t)G.rec;
   const int per = 8 / bits;
   // key groups [nblocks][H][d][nb]
   for (int i = tid; i < d * nb; i += blockDim.x) {
@@ -161,7 +161,7 @@ __global__ void k_export(Geo G, LayerBufs B, int seq, int nblocks, uint8_t* kcod
     kcodes[(((size_t)blk * G.H + h) * d + c) * nb + byte] = (uint8_t)v;
   }
   for (int c = tid; c < d; c += blockDim.x) {
-    GroupParams p = params_from_word(B.kparams[bi * d + kpi(G, c)], bits);
+    GroupParams p = params_from_word(B.kparams[bi * G.rec + kpi(G, c)], bits);
     size_t o = ((size_t)blk * G.H + h) * d + c;
     kzero[o] = double_to_half_bits_rn(p.zero);
     kscale[o] = double_to_half_bits_rn(p.scale);
@@ -181,7 +181,7 @@ __global__ void k_export(Geo G, LayerBufs B, int seq, int nblocks, uint8_t* kcod
   }
   for (int i = tid; i < g * G.nch; i += blockDim.x) {
     int t = i / G.nch, j = i - t * G.nch;
-    GroupParams p = params_from_word(B.vparams[bi * (size_t)(g * G.nch) + vpi(G, t, j)], bits);
+    GroupParams p = params_from_word(B.vparams[bi * (size_t)G.rec + vpi(G, t, j)], bits);
     size_t o = (((size_t)blk * g + t) * G.H + h) * G.nch + j;
     vzero[o] = double_to_half_bits_rn(p.zero);
     vscale[o] = double_to_half_bits_rn(p.scale);
@@ -202,21 +202,21 @@ __device__ inline float packed_key(const Geo& G, const LayerBufs& B, int b, int 
   int blk = pos / G.g, t = pos - blk * G.g;
   size_t bi = blk_index(G, b, h, blk);
   if (G.bits == 16)
-    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B.kcodes)[(bi * G.g + t) * G.d + c]);
+    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B.kcodes + bi * (size_t)G.rec)[t * G.d + c]);
   int w, bit;
   kloc(G, t, c, &w, &bit);
-  uint32_t code = read_code(B.kcodes + bi * (size_t)G.bwords, w, bit, G.bits);
-  return dequant_exact(code, params_from_word(B.kparams[bi * G.d + kpi(G, c)], G.bits));
+  uint32_t code = read_code(B.kcodes + bi * (size_t)G.rec, w, bit, G.bits);
+  return dequant_exact(code, params_from_word(B.kparams[bi * G.rec + kpi(G, c)], G.bits));
 }
 __device__ inline float packed_val(const Geo& G, const LayerBufs& B, int b, int h, int pos, int c) {
   int blk = pos / G.g, t = pos - blk * G.g;
   size_t bi = blk_index(G, b, h, blk);
   if (G.bits == 16)
-    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B.vcodes)[(bi * G.g + t) * G.d + c]);
+    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B.vcodes + bi * (size_t)G.rec)[t * G.d + c]);
   int w, bit;
   vloc(G, t, c, &w, &bit);
-  uint32_t code = read_code(B.vcodes + bi * (size_t)G.bwords, w, bit, G.bits);
-  return dequant_exact(code, params_from_word(B.vparams[bi * (size_t)(G.g * G.nch) + vpi(G, t, c / G.g)], G.bits));
+  uint32_t code = read_code(B.vcodes + bi * (size_t)G.rec, w, bit, G.bits);
+  return dequant_exact(code, params_from_word(B.vparams[bi * (size_t)G.rec + vpi(G, t, c / G.g)], G.bits));
 }
 
 __global__ void k_materialize(Geo G, LayerBufs B, int b, int h, int n, int f, float* keys,

@@ -240,50 +240,75 @@ void launch_set_pins(const Geo& G, const LayerBufs& B, int seq, int unit, const 
   k_set_pins<<<1, 256, 0, st>>>(G, B, seq, unit, pos, npos);
 }
 
-// K5: one CTA per (new-pin index, unit, seq).  Rows of a unit's heads are
-// contiguous in the host tier ([pos][H][d]), so a layer-scope pin moves one
-// contiguous H*d*2-byte K row and one V row with 16-byte zero-copy loads.
+// K5: PCIe gather of the new pins (zero-copy loads from the pinned host tier).
+// A small grid (kPfCtas CTAs per (seq, unit)) keeps SM slots free for K2 while
+// each thread keeps kPfUnroll independent 16-byte host loads in flight, enough
+// to cover PCIe latency at full link rate.  Rows of a unit's heads are
+// contiguous in the host tier ([pos][H][d]).
+constexpr int kPfCtas = 4;
+constexpr int kPfUnroll = 8;
+
 __global__ void __launch_bounds__(256) k_prefetch(Geo G, LayerBufs B, const uint4* host_k,
-                                                  const uint4* host_v, int seq0, int unit0) {
-  const int i = blockIdx.x, u = blockIdx.y + unit0, b = blockIdx.z + seq0;
+                                                  const uint4* host_v, int seq0, int unit0, int one) {
+  const int bu_i = one ? 0 : blockIdx.y;
+  const int u = one ? unit0 : bu_i % G.U, b = one ? seq0 : bu_i / G.U;
   const size_t bu = (size_t)b * G.U + u;
-  if (i >= B.newcnt[bu]) return;
-  const int slot = B.fetch_slot[bu * G.k + i], pos = B.fetch_pos[bu * G.k + i];
+  const int nnew = B.newcnt[bu];
   const int h0 = G.scope ? u : 0;
   if (G.d % 8) {  // small / odd head dims: element copies
     const __nv_bfloat16* hk = reinterpret_cast<const __nv_bfloat16*>(host_k);
     const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(host_v);
-    const size_t src = (((size_t)b * G.L + pos) * G.H + h0) * G.d;
-    const size_t dst = ((bu * G.k + slot) * G.Hu) * G.d;
-    for (int x = threadIdx.x; x < G.Hu * G.d; x += blockDim.x) {
-      B.pool_k[dst + x] = hk[src + x];
-      B.pool_v[dst + x] = hv[src + x];
+    const int row = G.Hu * G.d;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nnew * row; x += gridDim.x * blockDim.x) {
+      const int i = x / row, e = x - i * row;
+      const int slot = B.fetch_slot[bu * G.k + i], pos = B.fetch_pos[bu * G.k + i];
+      const size_t src = (((size_t)b * G.L + pos) * G.H + h0) * G.d + e;
+      const size_t dst = ((bu * G.k + slot) * G.Hu) * G.d + e;
+      B.pool_k[dst] = hk[src];
+      B.pool_v[dst] = hv[src];
     }
     return;
   }
   const int vec = G.Hu * G.d / 8;  // uint4 per row
-  const size_t src = (((size_t)b * G.L + pos) * G.H + h0) * G.d / 8;
-  const size_t dst = ((bu * G.k + slot) * G.Hu) * G.d / 8;
+  const int total = nnew * vec;
   uint4* pk = reinterpret_cast<uint4*>(B.pool_k);
   uint4* pv = reinterpret_cast<uint4*>(B.pool_v);
-  for (int x = threadIdx.x; x < vec; x += blockDim.x) {
-    uint4 a = host_k[src + x];
-    uint4 c = host_v[src + x];
-    pk[dst + x] = a;
-    pv[dst + x] = c;
+  const int stride = gridDim.x * blockDim.x;
+  for (int x0 = blockIdx.x * blockDim.x + threadIdx.x; x0 < total; x0 += stride * kPfUnroll) {
+    uint4 rk[kPfUnroll], rv[kPfUnroll];
+    size_t dst[kPfUnroll];
+#pragma unroll
+    for (int u2 = 0; u2 < kPfUnroll; ++u2) {
+      const int x = x0 + u2 * stride;
+      if (x < total) {
+        const int i = x / vec, e = x - i * vec;
+        const int slot = B.fetch_slot[bu * G.k + i], pos = B.fetch_pos[bu * G.k + i];
+        const size_t src = (((size_t)b * G.L + pos) * G.H + h0) * G.d / 8 + e;
+        dst[u2] = ((bu * G.k + slot) * G.Hu) * G.d / 8 + e;
+        rk[u2] = host_k[src];
+        rv[u2] = host_v[src];
+      }
+    }
+#pragma unroll
+    for (int u2 = 0; u2 < kPfUnroll; ++u2) {
+      if (x0 + u2 * stride < total) {
+        pk[dst[u2]] = rk[u2];
+        pv[dst[u2]] = rv[u2];
+      }
+    }
   }
 }
 
 void launch_prefetch(const Geo& G, const LayerBufs& B, const __nv_bfloat16* host_k,
                      const __nv_bfloat16* host_v, cudaStream_t st) {
-  k_prefetch<<<dim3(G.k, G.U, G.batch), 256, 0, st>>>(
-      G, B, reinterpret_cast<const uint4*>(host_k), reinterpret_cast<const uint4*>(host_v), 0, 0);
+  k_prefetch<<<dim3(kPfCtas, G.U * G.batch), 256, 0, st>>>(
+      G, B, reinterpret_cast<const uint4*>(host_k), reinterpret_cast<const uint4*>(host_v), 0, 0, 0);
 }
 
 void launch_prefetch_one(const Geo& G, const LayerBufs& B, int seq, int unit,
                          const __nv_bfloat16* host_k, const __nv_bfloat16* host_v, cudaStream_t st) {
-  k_prefetch<<<dim3(G.k, 1, 1), 256, 0, st>>>(
-      G, B, reinterpret_cast<const uint4*>(host_k), reinterpret_cast<const uint4*>(host_v), seq, unit);
+  k_prefetch<<<dim3(kPfCtas, 1), 256, 0, st>>>(
+      G, B, reinterpret_cast<const uint4*>(host_k), reinterpret_cast<const uint4*>(host_v), seq, unit, 1);
 }
 
 // pin() with caller-supplied rows: device bf16 [npos][Hu][d] -> slots 0..npos-1
