@@ -64,6 +64,24 @@ def dist_env():
     return rank, world, local, local_world
 
 
+def reduce_max(value: float, device=None) -> float:
+    """Max over ranks (the timing rule: a multi-GPU number is the slowest rank)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64,
+                     device=device if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_tokens(batch: int, steps: int, world: int) -> int:
+    """Every rank decodes its own `batch` sequences (sequence sharding, weak
+    scaling); one verified token per sequence per step (engine.py:172)."""
+    return batch * steps * world
+
+
 def mem_available_bytes() -> int:
     try:
         with open("/proc/meminfo") as fh:
@@ -353,10 +371,8 @@ def run_gpu_arm(args, cfg):
     _, newc = dec.ticket(L // 2)
     npin = int((picked0 >= 0).sum().item()) // max(1, cfg["batch"])
     new_frac = float(newc.float().mean().item()) / max(1, cfg["topk"])
+    elapsed_ms = reduce_max(elapsed_ms, device)
     if world > 1:
-        tt = torch.tensor([elapsed_ms], device=device)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(tt.item())
         dist.barrier()
 
     # ---- end-to-end: host buffers in, host results out, copies inside the region ----
@@ -389,15 +405,12 @@ def run_gpu_arm(args, cfg):
         t += 1
     torch.cuda.synchronize(device)
     e2e_s = time.perf_counter() - w0
-    if world > 1:
-        tt = torch.tensor([e2e_s], device=device)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+    e2e_s = reduce_max(e2e_s, device)
     h2d = (q_d.numel() + k_d.numel() + v_d.numel()) * 2
     d2h = o_h.numel() * 2 + pm_h.numel() * 4
 
     ms_per_step = elapsed_ms / K
-    tokens = cfg["batch"] * K * world
+    tokens = whole_job_tokens(cfg["batch"], K, world)
     value = tokens / (elapsed_ms / 1e3)
     ab = algorithmic_bytes_per_layer(cfg, n_mid + K // 2, f_mid, npin)
     attn_avg_ms = attn_ms / max(1, attn_n)
@@ -435,7 +448,7 @@ def run_gpu_arm(args, cfg):
                      "launches": attn_n, "kernel_share_of_step": attn_ms / max(1e-9, elapsed_ms)},
         "prefetch": {"new_pin_fraction": new_frac, "h2d_bytes_per_step": h2d_pf,
                      "copy_stream_ms_per_step": sel_ms / K, "h2d_gbs_if_serial": (h2d_pf / 1e9) / max(1e-9, sel_ms / K / 1e3)},
-        "e2e": {"value": tokens / e2e_s if world == 1 else cfg["batch"] * K * world / e2e_s,
+        "e2e": {"value": tokens / e2e_s,
                 "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clocks.summary(),

@@ -1,0 +1,101 @@
+"""Multi-process (gloo, world size 2) coverage of the N>1 path on CPU.
+
+bench.py shards the decode by sequence with no data-path collective: each
+rank owns its sequences' caches.  These tests check, with the oracle as the
+compute stand-in, that (1) per-rank sharded decode results equal a
+single-process run (the path is exchange-free under sequence sharding, incl.
+the layer-scope top-k), and (2) the timing/aggregation helpers of bench.py
+reduce with MAX over ranks and count whole-job tokens.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import restate as R
+from oracle.synth import make_kv, make_queries, make_step_kv
+
+WORLD = 2
+CFG = dict(n0=300, H=2, Hq=4, d=16, bits=2, g=8, r=8, k=6, seqs=4)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _seq_inputs(seq):
+    rng = np.random.default_rng(100 + seq)
+    K, V = make_kv(rng, CFG["n0"], CFG["H"], CFG["d"])
+    q = make_queries(rng, 2, CFG["Hq"], CFG["d"])
+    kn, vn = make_step_kv(rng, 2, CFG["H"], CFG["d"])
+    return K, V, q, kn, vn
+
+
+def _decode_seq(seq):
+    K, V, q, kn, vn = _seq_inputs(seq)
+    st = R.LayerState(CFG["H"], CFG["d"], CFG["bits"], CFG["g"], CFG["r"], CFG["k"])
+    st.extend(K, V)
+    res = R.decode_layer(st, q, kn, vn)
+    picked = np.full(CFG["k"], -1, np.int64)
+    picked[:len(res["picked"][0])] = res["picked"][0]
+    return res["out"].astype(np.float32), picked
+
+
+def _worker(rank, port, out_q):
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    mine = list(range(rank, CFG["seqs"], WORLD))            # sequence sharding
+    outs = {s: _decode_seq(s) for s in mine}
+    gathered = [None] * WORLD
+    dist.all_gather_object(gathered, outs)
+    # bench.py aggregation: MAX of per-rank elapsed, whole-job tokens
+    import bench
+    elapsed = torch.tensor([10.0 + rank], dtype=torch.float64)
+    mx = bench.reduce_max(elapsed.item())
+    tokens = bench.whole_job_tokens(batch=len(mine), steps=5, world=WORLD)
+    if rank == 0:
+        merged = {}
+        for g in gathered:
+            merged.update(g)
+        out_q.put((merged, mx, tokens))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sequence_sharding_is_exchange_free_and_max_reduced():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    merged, mx, tokens = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert mx == 11.0
+    assert tokens == 2 * 5 * WORLD
+    for s in range(CFG["seqs"]):
+        out, picked = _decode_seq(s)
+        np.testing.assert_array_equal(merged[s][0], out)
+        np.testing.assert_array_equal(merged[s][1], picked)
+
+
+def test_plan_host_layers():
+    import bench
+    cfg = dict(bench.CONFIGS["c2"])
+    slab = 2 * cfg["batch"] * (cfg["ctx"] + 256) * cfg["kv_heads"] * cfg["head_dim"] * 2
+    # 196 GB box, 1 rank: largest divisor of 32 layers within 45% of available
+    hl = bench.plan_host_layers(cfg, 1, avail=196 << 30)
+    assert cfg["layers"] % hl == 0 and hl * slab <= 0.45 * (196 << 30)
+    assert bench.plan_host_layers(cfg, 8, avail=196 << 30) == 1
+    assert bench.plan_host_layers(cfg, 1, avail=4 << 40) == 32
