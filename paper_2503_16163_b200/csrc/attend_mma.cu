@@ -39,6 +39,7 @@
 // The last split is the exact segment (pinned slots, residual window, in-step
 // rows; full-precision bf16 rows, fp32 CUDA-core dot products).
 #include <algorithm>
+#include <cstdlib>
 
 #include "exact_segment.cuh"
 
@@ -499,8 +500,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         }
         ws.bk[kks][(4 * j + ktk) ^ kks] = frag;
       }
+      if (NR == 2) {
+        // two-row reduce-scatter: after the first exchange lanes with bit4 == j
+        // carry row j; four more butterflies finish both rows (6 SHFL, not 10)
+        const bool hi16 = lane & 16;
+        float mine = hi16 ? Cp[1] : Cp[0];
+        const float other = hi16 ? Cp[0] : Cp[1];
+        mine += __shfl_xor_sync(0xffffffffu, other, 16);
 #pragma unroll
-      for (int j = 0; j < NR; ++j) Cp[j] = warp_sum_all(Cp[j]);
+        for (int o = 8; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+        Cp[0] = __shfl_sync(0xffffffffu, mine, 0);
+        Cp[1] = __shfl_sync(0xffffffffu, mine, 16);
+      } else {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) Cp[j] = warp_sum_all(Cp[j]);
+      }
     }
     // key codes of this lane's tokens T0 = 16mt + gq, T1 = T0 + 8
     uint32_t kw[2][2 * BITS];
@@ -584,17 +598,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
-        const int T = 16 * mt + gq + 8 * hf;
-        const bool msk = (bm >> T) & 1u;
 #pragma unroll
         for (int e = 0; e < RPL; ++e) {
           float d;
           if (PACK) d = (dk[mt][2 * hf] + dl[mt][2 * hf]) + (dk[mt][2 * hf + 1] + dl[mt][2 * hf + 1]);
           else d = dk[mt][2 * hf + e] + dl[mt][2 * hf + e];
-          const float s = fmaf(d, k_out, cr[e]);
-          sc[mt][hf][e] = msk ? -CUDART_INF_F : s;
-          if (!msk && spr[e]) spr[e][pos0 + T] = s;
+          sc[mt][hf][e] = fmaf(d, k_out, cr[e]);
         }
+      }
+    }
+    if (bm) {  // pinned positions are attended from their exact rows (exact segment)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf)
+          if ((bm >> (16 * mt + gq + 8 * hf)) & 1u) {
+#pragma unroll
+            for (int e = 0; e < RPL; ++e) sc[mt][hf][e] = -CUDART_INF_F;
+          }
+    }
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) {
+      if (spr[e]) {  // aggregate-row logits (one writer per position: pinned ones by the exact segment)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            const int T = 16 * mt + gq + 8 * hf;
+            if (!((bm >> T) & 1u)) spr[e][pos0 + T] = sc[mt][hf][e];
+          }
       }
     }
     float mn[RPL];
@@ -843,472 +875,6 @@ void launch_fast_t(const AttnArgs& a, cudaStream_t st) {
 }
 
 
-// ======================================================================================
-// Warp-specialized variant (MHA: NR <= 2).  Each CTA runs kPairs (key warp, value
-// warp) pairs.  The key warp of a pair builds the key B fragments, runs the score
-// MMAs and the online softmax, and hands P (+ the per-row rescale factor) to its
-// value warp through a double-buffered shared buffer guarded by mbarriers
-// (pfull: key -> value, pempty: value -> key).  The value warp builds the P.V B
-// fragments, runs the P.V MMAs and refills the pair's TMA stage once it has read
-// it (it is the stage's last reader).  Splitting the per-block state between two
-// warps roughly halves per-thread registers (3 CTAs = 24 warps per SM instead of
-// 16) and gives each SM two independent instruction streams per block.
-constexpr int kPairs = 4;
-
-template <int BITS, int NR>
-struct __align__(16) PairSmem {
-  uint4 bk[8][32];                                    // key warp: key B fragments
-  uint32_t stage[kStages][StageLayout<BITS>::words];  // TMA ring (both warps read)
-  float P[2][NR][33];                                 // key -> value probabilities
-  float alpha[2][NR];                                 // per-row rescale of the block
-  uint64_t full[kStages];
-  uint64_t pfull[2];
-  uint64_t pempty[2];
-};
-
-template <int NR>
-struct MergeSmemP {
-  float o[kPairs][NR][128];
-  float m[kPairs][NR];
-  float l[kPairs][NR];
-};
-
-template <int BITS, int NR>
-constexpr size_t ws_smem_bytes() {
-  size_t a = sizeof(PairSmem<BITS, NR>) * kPairs, b = sizeof(MergeSmemP<NR>), c = sizeof(ExactSmem<NR>);
-  return a > b ? (a > c ? a : c) : (b > c ? b : c);
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-template <int BITS, int NR>
-__global__ void __launch_bounds__(kThreads, 3) k_attend_ws(AttnArgs a) {
-  static_assert(NR <= 2, "warp-specialized path serves MHA (<= 2 rows)");
-  using SL = StageLayout<BITS>;
-  const Geo& G = a.G;
-  const LayerBufs& B = a.B;
-  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  if (split == a.nsplit) {
-    exact_segment_fast<NR>(a, split, h, b, smem_raw);
-    return;
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pair = warp & (kPairs - 1), role = warp >> 2;  // role 0: key warp, 1: value warp
-  const int gq = lane >> 2, tq = lane & 3;
-  PairSmem<BITS, NR>& ps = reinterpret_cast<PairSmem<BITS, NR>*>(smem_raw)[pair];
-
-  const int nb_total = a.f / 32;
-  const int blk0 = split * a.blocks_per_split;
-  const int blk1 = min(nb_total, blk0 + a.blocks_per_split);
-  const float cs = BITS == 1 ? 0.5f : (1.f / 3.f);
-  const size_t bi0 = blk_index(G, b, h, 0);
-  const uint32_t* rec_base = B.kcodes + bi0 * (size_t)SL::words;
-
-  if (role == 1 && lane == 0) {
-#pragma unroll
-    for (int s = 0; s < kStages; ++s) mbar_init(&ps.full[s], 1);
-    mbar_init(&ps.pfull[0], 1);
-    mbar_init(&ps.pfull[1], 1);
-    mbar_init(&ps.pempty[0], 1);
-    mbar_init(&ps.pempty[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-
-  float m_run = -CUDART_INF_F, l_run = 0.f;  // key warp: score row tq
-  float dv[8][4];                            // value warp accumulators
-  float zacc = 0.f;
-
-  if (role == 0) {
-    // ================================ key warp ========================================
-    const int kks = lane & 7, ktk = lane >> 3;
-    float Qr[NR][4];
-    float qabs = 0.f;
-#pragma unroll
-    for (int j = 0; j < NR; ++j) {
-      const int r = j / G.G, g2 = j - r * G.G;
-      const __nv_bfloat16* qp = a.q + (((size_t)b * a.rows + r) * G.Hq + h * G.G + g2) * 128;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        Qr[j][m] = __bfloat162float(qp[32 * ktk + kks + 8 * m]) * a.sm_scale_log2;
-        qabs = fmaxf(qabs, fabsf(Qr[j][m]));
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) qabs = fmaxf(qabs, __shfl_xor_sync(0xffffffffu, qabs, o));
-    const float rk = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 2 + 0]) * cs;
-    const int Ek = (qabs * rk > 0.f) ? ceil_log2(qabs * rk) - 14 : 0;
-    const int sp = BITS == 2 ? 2 * (kks & 3) : kks;
-    const float kscale = cs * pow2i(-sp - Ek);
-    const float k_out = pow2i(24 + Ek);
-    const int agg_j0 = a.agg_row * G.G;
-    const int jr = tq;  // PACK: one score row per lane
-    float* spr = (jr < NR && jr >= agg_j0 && jr < agg_j0 + G.G)
-                     ? a.spill + ((size_t)b * G.Hq + h * G.G + (jr - agg_j0)) * G.L : nullptr;
-    const uint32_t* bm_base = B.bitmap + ((size_t)b * G.U + (G.scope ? h : 0)) * (G.L / 32);
-    for (int i = lane; i < 8 * 32; i += 32) {
-      const int ks = i >> 5, l = i & 31;
-      if ((l >> 2) >= NR) ps.bk[ks][l ^ ks] = make_uint4(0, 0, 0, 0);
-    }
-    int st = 0, i = 0;
-    unsigned phase = 0;
-    uint32_t bm = (blk0 + pair < blk1) ? bm_base[blk0 + pair] : 0u;
-    for (int blk = blk0 + pair; blk < blk1; blk += kPairs, ++i) {
-      const uint32_t nbm = (blk + kPairs < blk1) ? bm_base[blk + kPairs] : 0u;
-      mbar_wait(&ps.full[st], phase);
-      const uint32_t* S = ps.stage[st];
-      // key B fragments + C_j (lane (kks, ktk): channels 32ktk + kks + 8m)
-      float Cp[NR];
-      {
-        const uint4 kp4 = *reinterpret_cast<const uint4*>(S + SL::kp + 4 * lane);
-        const uint32_t kpw[4] = {kp4.x, kp4.y, kp4.z, kp4.w};
-        float s4[4], z4[4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const float lo = __uint_as_float(kpw[m] << 16), hi = __uint_as_float(kpw[m] & 0xFFFF0000u);
-          s4[m] = (hi - lo) * kscale;
-          z4[m] = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
-        }
-#pragma unroll
-        for (int j = 0; j < NR; ++j) {
-          const float w0 = Qr[j][0] * s4[0], w1 = Qr[j][1] * s4[1], w2 = Qr[j][2] * s4[2],
-                      w3 = Qr[j][3] * s4[3];
-          Cp[j] = fmaf(Qr[j][0], z4[0], fmaf(Qr[j][1], z4[1], fmaf(Qr[j][2], z4[2], Qr[j][3] * z4[3])));
-          uint4 frag;
-          if (BITS == 2) {
-            split2(w0, w1, frag.x, frag.z);
-            split2(w2, w3, frag.y, frag.w);
-          } else {
-            split2(w0, w2, frag.x, frag.z);
-            split2(w1, w3, frag.y, frag.w);
-          }
-          ps.bk[kks][(4 * j + ktk) ^ kks] = frag;
-        }
-      }
-      // C of this lane's score row: NR-way reduce-scatter + broadcast
-      float cr;
-      if (NR == 1) {
-        cr = warp_sum_all(Cp[0]);
-      } else {
-        // after step 1 lanes with bit4 == j hold row j, summed over lane pairs (l, l^16)
-        const bool hi16 = lane & 16;
-        float mine = hi16 ? Cp[NR - 1] : Cp[0], other = hi16 ? Cp[0] : Cp[NR - 1];
-        mine += __shfl_xor_sync(0xffffffffu, other, 16);
-#pragma unroll
-        for (int o = 8; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-        cr = __shfl_sync(0xffffffffu, mine, (tq & 1) << 4);  // row tq (tq < NR)
-      }
-      uint32_t kw[2][2 * BITS];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          const int T = 16 * mt + gq + 8 * hf;
-          if (BITS == 2) {
-            const uint2 w = *reinterpret_cast<const uint2*>(S + SL::kc + T * 8 + 2 * tq);
-            kw[mt][2 * hf] = w.x;
-            kw[mt][2 * hf + 1] = w.y;
-          } else {
-            kw[mt][hf] = S[SL::kc + T * 4 + tq];
-          }
-        }
-      }
-      __syncwarp();
-      float dk[2][4], dl[2][4];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int x = 0; x < 4; ++x) dk[mt][x] = dl[mt][x] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const uint2 bb = reinterpret_cast<const uint2*>(&ps.bk[ks][(4 * (gq >> 1) + tq) ^ ks])[gq & 1];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          uint32_t a0, a1, a2, a3;
-          if (BITS == 2) {
-            const uint32_t msk = (3u << (2 * (ks & 3))) | (3u << (16 + 2 * (ks & 3)));
-            const int sh = ks < 4 ? 0 : 8;
-            a0 = (kw[mt][0] >> sh) & msk;
-            a2 = (kw[mt][1] >> sh) & msk;
-            a1 = (kw[mt][2] >> sh) & msk;
-            a3 = (kw[mt][3] >> sh) & msk;
-          } else {
-            const uint32_t msk = (1u << ks) | (1u << (16 + ks));
-            a0 = kw[mt][0] & msk;
-            a2 = (kw[mt][0] >> 8) & msk;
-            a1 = kw[mt][1] & msk;
-            a3 = (kw[mt][1] >> 8) & msk;
-          }
-          if (ks & 1) mma16816(dl[mt], a0, a1, a2, a3, bb.x, bb.y);
-          else mma16816(dk[mt], a0, a1, a2, a3, bb.x, bb.y);
-        }
-      }
-      // epilogue
-      float sc[2][2];
-      const int pos0 = blk * 32;
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          const float d = (dk[mt][2 * hf] + dl[mt][2 * hf]) + (dk[mt][2 * hf + 1] + dl[mt][2 * hf + 1]);
-          sc[mt][hf] = fmaf(d, k_out, cr);
-        }
-      }
-      if (bm) {  // pinned positions are attended from their exact rows instead
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf)
-            if ((bm >> (16 * mt + gq + 8 * hf)) & 1u) sc[mt][hf] = -CUDART_INF_F;
-      }
-      if (spr) {
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            const int T = 16 * mt + gq + 8 * hf;
-            if (!((bm >> T) & 1u)) spr[pos0 + T] = sc[mt][hf];
-          }
-      }
-      float mx = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
-      mx = warp_max_g(mx);
-      const float mn = fmaxf(m_run, mx);
-      float al = 1.f;
-      if (mn > m_run) {
-        al = m_run == -CUDART_INF_F ? 0.f : fast_exp2(m_run - mn);
-        l_run *= al;
-        m_run = mn;
-      }
-      const int pb = i & 1;
-      if (i >= 2) mbar_wait(&ps.pempty[pb], ((i - 2) >> 1) & 1);
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          const float p = fast_exp2(sc[mt][hf] - m_run);
-          l_run += p;
-          if (jr < NR) ps.P[pb][jr][16 * mt + gq + 8 * hf] = p;
-        }
-      }
-      if (gq == 0 && jr < NR) ps.alpha[pb][jr] = al;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ps.pfull[pb]);
-      bm = nbm;
-      if (++st == kStages) {
-        st = 0;
-        phase ^= 1u;
-      }
-    }
-    l_run = warp_sum_g(l_run);
-  } else {
-    // =============================== value warp ========================================
-    const float rv = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 2 + 1]) * cs;
-    const int Ev = (rv > 0.f) ? ceil_log2(rv) - 14 : 0;
-    float vscale[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) vscale[q] = cs * pow2i(-(BITS == 2 ? 2 * q : q) - Ev);
-    // PG role: column n = gq -> (grp = gq / NR, row = gq % NR)
-    const int grp = (gq / NR) & 3, vrow = gq % NR;
-    const bool live = gq < 4 * NR;
-    const int c0r = (2 * tq) % NR, c1r = (2 * tq + 1) % NR;  // rows of this lane's D columns
-#pragma unroll
-    for (int x = 0; x < 8; ++x) dv[x][0] = dv[x][1] = dv[x][2] = dv[x][3] = 0.f;
-    if (lane == 0) {
-#pragma unroll
-      for (int s = 0; s < kStages; ++s) {
-        const int blk = blk0 + pair + s * kPairs;
-        if (blk < blk1) {
-          mbar_expect_tx(&ps.full[s], SL::bytes);
-          tma_load(ps.stage[s], rec_base + (size_t)blk * SL::words, SL::bytes, &ps.full[s]);
-        }
-      }
-    }
-    __syncwarp();
-    int st = 0, i = 0;
-    unsigned phase = 0;
-    for (int blk = blk0 + pair; blk < blk1; blk += kPairs, ++i) {
-      mbar_wait(&ps.full[st], phase);
-      const uint32_t* S = ps.stage[st];
-      uint32_t vw[4 * BITS];
-      {
-        const uint4 w0 = *reinterpret_cast<const uint4*>(S + SL::vc + lane * 4);
-        vw[0] = w0.x;
-        vw[1] = w0.y;
-        vw[2] = w0.z;
-        vw[3] = w0.w;
-        if (BITS == 2) {
-          const uint4 w1 = *reinterpret_cast<const uint4*>(S + SL::vc + 128 + lane * 4);
-          vw[4 % (4 * BITS)] = w1.x;
-          vw[5 % (4 * BITS)] = w1.y;
-          vw[6 % (4 * BITS)] = w1.z;
-          vw[7 % (4 * BITS)] = w1.w;
-        }
-      }
-      // value params of this lane's tokens (independent of P: overlaps the wait)
-      const uint4 v0 = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * grp + 8 * tq);
-      const uint4 v1 = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * grp + 8 * tq + 4);
-      const uint32_t vpw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      float sv[8], zv[8];
-#pragma unroll
-      for (int x = 0; x < 8; ++x) {
-        const float lo = __uint_as_float(vpw[x] << 16), hi = __uint_as_float(vpw[x] & 0xFFFF0000u);
-        sv[x] = (hi - lo) * vscale[2 * (x >> 2) + ((x >> 1) & 1)];
-        zv[x] = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
-      }
-      const int pb = i & 1;
-      mbar_wait(&ps.pfull[pb], (i >> 1) & 1);
-      const float a0r = ps.alpha[pb][c0r], a1r = ps.alpha[pb][c1r], azr = ps.alpha[pb][vrow];
-      if (a0r != 1.f || a1r != 1.f) {  // online-softmax rescale (uniform across the warp)
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          dv[mt][0] *= a0r;
-          dv[mt][1] *= a1r;
-          dv[mt][2] *= a0r;
-          dv[mt][3] *= a1r;
-        }
-      }
-      zacc *= azr;
-      uint32_t vb[2][4];  // [ks] {b0hi, b1hi, b0lo, b1lo}
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        float x[4];
-#pragma unroll
-        for (int slot = 0; slot < 4; ++slot) {
-          const int t = 16 * ks + 2 * tq + (slot & 1) + 8 * (slot >> 1);
-          const float p = live ? ps.P[pb][vrow][t] : 0.f;
-          zacc = fmaf(p, zv[4 * ks + slot], zacc);
-          x[slot] = p * sv[4 * ks + slot];
-        }
-        split2(x[0], x[1], vb[ks][0], vb[ks][2]);
-        split2(x[2], x[3], vb[ks][1], vb[ks][3]);
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&ps.pempty[pb]);
-        const int nblk = blk + kStages * kPairs;  // refill: this warp is the stage's last reader
-        if (nblk < blk1) {
-          fence_proxy_async();
-          mbar_expect_tx(&ps.full[st], SL::bytes);
-          tma_load(ps.stage[st], rec_base + (size_t)nblk * SL::words, SL::bytes, &ps.full[st]);
-        }
-      }
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          uint32_t a0, a1, a2, a3;
-          const int q0 = 2 * ks, q1 = 2 * ks + 1;
-          if (BITS == 2) {
-            const uint32_t W = vw[mt % (4 * BITS)], W8 = W >> 8;
-            const uint32_t m0 = (3u << (2 * q0)) | (3u << (16 + 2 * q0));
-            const uint32_t m1 = (3u << (2 * q1)) | (3u << (16 + 2 * q1));
-            a0 = W & m0;
-            a1 = W8 & m0;
-            a2 = W & m1;
-            a3 = W8 & m1;
-          } else {
-            const uint32_t W = vw[(mt >> 1) % (4 * BITS)] >> (8 * (mt & 1)), W4 = W >> 4;
-            const uint32_t m0 = (1u << q0) | (1u << (16 + q0));
-            const uint32_t m1 = (1u << q1) | (1u << (16 + q1));
-            a0 = W & m0;
-            a1 = W4 & m0;
-            a2 = W & m1;
-            a3 = W4 & m1;
-          }
-          mma16816(dv[mt], a0, a1, a2, a3, vb[ks][0], vb[ks][1]);
-          mma16816(dv[mt], a0, a1, a2, a3, vb[ks][2], vb[ks][3]);
-        }
-      }
-      if (++st == kStages) {
-        st = 0;
-        phase ^= 1u;
-      }
-    }
-    zacc += __shfl_xor_sync(0xffffffffu, zacc, 1);
-    zacc += __shfl_xor_sync(0xffffffffu, zacc, 2);
-  }
-
-  // ---- pair results -> shared, CTA merge -> partial -----------------------------------
-  __syncthreads();
-  if (role == 1 && lane == 0) {
-#pragma unroll
-    for (int s = 0; s < kStages; ++s)
-      asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&ps.full[s])) : "memory");
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&ps.pfull[s])) : "memory");
-      asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&ps.pempty[s])) : "memory");
-    }
-  }
-  __syncthreads();
-  MergeSmemP<NR>& ms = *reinterpret_cast<MergeSmemP<NR>*>(smem_raw);
-  if (role == 0) {
-    if (gq == 0 && tq < NR) {
-      ms.m[pair][tq] = m_run;
-      ms.l[pair][tq] = l_run;
-    }
-  } else {
-    const float v_out_unused = 0.f;
-    (void)v_out_unused;
-    const float rv = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 2 + 1]) * cs;
-    const int Ev = (rv > 0.f) ? ceil_log2(rv) - 14 : 0;
-    const float v_out = pow2i(24 + Ev);
-    const float zc0 = __shfl_sync(0xffffffffu, zacc, 4 * (2 * tq));
-    const float zc1 = __shfl_sync(0xffffffffu, zacc, 4 * ((2 * tq + 1) & 7));
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int n = 2 * tq + e;
-        if (n < 4 * NR && n / NR == (mt >> 1)) {
-          const int j = n % NR;
-          const float zc = e ? zc1 : zc0;
-          ms.o[pair][j][16 * mt + gq] = fmaf(dv[mt][e], v_out, zc);
-          ms.o[pair][j][16 * mt + gq + 8] = fmaf(dv[mt][2 + e], v_out, zc);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  const size_t base = (((size_t)b * G.H + h) * (a.nsplit + 1) + split) * NR;
-  for (int x = threadIdx.x; x < NR * 128; x += kThreads) {
-    const int j = x >> 7, c = x & 127;
-    float M = -CUDART_INF_F;
-#pragma unroll
-    for (int w = 0; w < kPairs; ++w)
-      if (ms.l[w][j] > 0.f) M = fmaxf(M, ms.m[w][j]);
-    float o = 0.f, L = 0.f;
-#pragma unroll
-    for (int w = 0; w < kPairs; ++w) {
-      if (ms.l[w][j] > 0.f) {
-        const float f = exp2f(ms.m[w][j] - M);
-        o = fmaf(ms.o[w][j][c], f, o);
-        L = fmaf(ms.l[w][j], f, L);
-      }
-    }
-    a.part_o[(base + j) * 128 + c] = o;
-    if (c == 0) {
-      a.part_ml[(base + j) * 2 + 0] = M;
-      a.part_ml[(base + j) * 2 + 1] = L;
-    }
-  }
-}
-
-template <int BITS, int NR>
-void launch_ws_t(const AttnArgs& a, cudaStream_t st) {
-  constexpr size_t smem = ws_smem_bytes<BITS, NR>();
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_attend_ws<BITS, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
-  dim3 grid(a.nsplit + 1, a.G.H, a.G.batch);
-  k_attend_ws<BITS, NR><<<grid, kThreads, smem, st>>>(a);
-}
-
 }  // namespace
 
 int attend_fast_supported(const Geo& G, int rows) {
@@ -1322,19 +888,23 @@ int launch_attend_fast(const AttnArgs& a0, cudaStream_t st) {
   const Geo& G = a.G;
   const int nblk = a.f / 32;
   const int units = G.H * G.batch;
-  int want = (6 * 2 * 148 + units - 1) / units;  // ~6 waves
+  static const int waves = [] {
+    const char* e = getenv("SPC_SPLIT_WAVES");
+    return e ? std::max(1, atoi(e)) : 6;
+  }();
+  int want = (waves * 2 * 148 + units - 1) / units;  // ~`waves` waves at 2 CTAs/SM
   want = std::max(1, std::min(want, std::min(127, std::max(1, nblk / 8))));
   a.blocks_per_split = std::max(1, (nblk + want - 1) / want);
   a.nsplit = std::max(1, (nblk + a.blocks_per_split - 1) / a.blocks_per_split);
   const int R = a.rows * G.G;
   if (G.bits == 2) {
-    if (R == 1) launch_ws_t<2, 1>(a, st);
-    else if (R == 2) launch_ws_t<2, 2>(a, st);
+    if (R == 1) launch_fast_t<2, 1>(a, st);
+    else if (R == 2) launch_fast_t<2, 2>(a, st);
     else if (R == 4) launch_fast_t<2, 4>(a, st);
     else launch_fast_t<2, 8>(a, st);
   } else {
-    if (R == 1) launch_ws_t<1, 1>(a, st);
-    else if (R == 2) launch_ws_t<1, 2>(a, st);
+    if (R == 1) launch_fast_t<1, 1>(a, st);
+    else if (R == 2) launch_fast_t<1, 2>(a, st);
     else if (R == 4) launch_fast_t<1, 4>(a, st);
     else launch_fast_t<1, 8>(a, st);
   }
