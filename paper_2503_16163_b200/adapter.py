@@ -1,0 +1,260 @@
+"""DeviceSpeculativeDecoder -- drop-in for the reference's token loop
+(SpeculativeDecoder / generate, engine.py:186-386) with the SpeCache hot path
+on the B200 (DeviceTwoTierCache + SpeculativeLayerDecoder).
+
+This is the SURVEY.md 8(f) "next" row 2: it closes the loop from prompt to
+tokens so the object-level API of the reference can be driven on the device.
+The toy model around the hot path (RMSNorm, projections, RoPE, SiLU FFN,
+logits; engine.py:35-72, numerics.py:42-78) runs as plain fp32 PyTorch on the
+same GPU -- it is plumbing around the path, not part of it.  The hot-path
+boundary is bf16: q/k/v enter the cache and the attention as bf16, attention
+outputs leave as bf16 (the C ABI contract).
+
+Same constructor arguments, phase rules (ProtocolError), StepMetrics and
+GenerateResult fields as the reference; the transfer-latency report rows use
+the reference's logical-clock model (transfer.py:58-112).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .budget import CacheBudget
+from .cache import DeviceTwoTierCache
+from .decode import SpeculativeLayerDecoder, StepMetrics
+from .transfer import ChannelModel, ProtocolError, step_latency, transfer_time
+
+__all__ = ["DeviceSpeculativeDecoder", "GenerateResult", "generate"]
+
+
+@dataclass
+class GenerateResult:
+    """engine.py:175-183."""
+    tokens: list
+    logits: list
+    metrics: list
+    latency_rows: list
+    prefill_seconds: float
+    total_seconds: float
+    decoder: "DeviceSpeculativeDecoder" = None
+
+
+class DeviceSpeculativeDecoder:
+    """engine.py:186-339 on the device cache.  `config` / `weights` are the
+    reference's DecoderConfig / Weights (or any objects with the same fields)."""
+
+    def __init__(self, config, weights, budget: CacheBudget, channel_model: ChannelModel | None = None,
+                 mode: str = "sim", compute_time_per_step: float = 0.0, prefill_time: float = 0.0,
+                 device: int = 0):
+        import torch
+        if mode not in ("sim", "thread"):
+            raise ValueError("mode must be 'sim' or 'thread'")
+        torch.backends.cuda.matmul.allow_tf32 = False  # fp32 model math, as the reference
+        self.config, self.budget = config, budget
+        self.dev = f"cuda:{device}"
+        T = lambda a: torch.as_tensor(np.asarray(a, np.float32), device=self.dev)
+        self.emb = T(weights.embedding)
+        self.lw = [{k: T(getattr(lw, k)) for k in ("wq", "wk", "wv", "wo", "attn_norm", "ffn_norm", "w1", "w2")}
+                   for lw in weights.layers]
+        self.final_norm, self.head = T(weights.final_norm), T(weights.head)
+        self.cache = DeviceTwoTierCache(config.layers, config.kv_heads, config.head_dim, budget,
+                                        q_heads=config.q_heads, device=device)
+        self.layer_dec = SpeculativeLayerDecoder(self.cache)
+        self.channel_model = channel_model or ChannelModel()
+        self.compute_time_per_step = compute_time_per_step
+        self.prefill_time = prefill_time
+        self.clock = 0.0
+        self._step_seconds: dict[int, float] = {}
+        self._phase = "init"
+        self._step = 0
+        self._pos = 0
+        self._verified = None
+        self._speculative = None
+        self.predecode_bytes = 0
+        self.predecode_new_pins = 0
+        self.last_logits = None
+        d = config.head_dim
+        idx = np.arange(d // 2, dtype=np.float64)
+        self._inv_freq = config.rope_base ** (-2.0 * idx / d)
+
+    def close(self) -> None:
+        self.cache.close()
+
+    # -- toy model pieces (fp32, on device) ---------------------------------------------
+    def _rmsnorm(self, x, gain, eps=1e-6):
+        import torch
+        ms = torch.mean(x * x, dim=-1, keepdim=True)
+        return x * gain / torch.sqrt(ms + eps)
+
+    def _rope(self, x, positions):
+        import torch
+        ang = np.outer(np.asarray(positions, np.float64), self._inv_freq)  # float64 like numerics.py:62
+        cos = torch.as_tensor(np.cos(ang).astype(np.float32), device=self.dev)[:, None, :]
+        sin = torch.as_tensor(np.sin(ang).astype(np.float32), device=self.dev)[:, None, :]
+        x0, x1 = x[..., 0::2], x[..., 1::2]
+        out = torch.empty_like(x)
+        out[..., 0::2] = x0 * cos - x1 * sin
+        out[..., 1::2] = x0 * sin + x1 * cos
+        return out
+
+    def _qkv(self, lw, x, positions):
+        """engine.py:39-48, then rounded to bf16 at the hot-path boundary."""
+        import torch
+        cfg = self.config
+        n = x.shape[0]
+        xn = self._rmsnorm(x, lw["attn_norm"])
+        q = (xn @ lw["wq"]).reshape(n, cfg.q_heads, cfg.head_dim)
+        k = (xn @ lw["wk"]).reshape(n, cfg.kv_heads, cfg.head_dim)
+        v = (xn @ lw["wv"]).reshape(n, cfg.kv_heads, cfg.head_dim)
+        q, k = self._rope(q, positions), self._rope(k, positions)
+        bf = lambda t: t.to(torch.bfloat16)
+        return bf(q), bf(k), bf(v)
+
+    def _ffn(self, lw, x):
+        import torch
+        xn = self._rmsnorm(x, lw["ffn_norm"])
+        g = xn @ lw["w1"]
+        return x + (g / (1.0 + torch.exp(-g))) @ lw["w2"]
+
+    def _logits(self, x):
+        return self._rmsnorm(x, self.final_norm) @ self.head
+
+    # -- phases (engine.py:220-339) --------------------------------------------------------
+    def prefill(self, prompt) -> int:
+        import torch
+        if self._phase != "init":
+            raise ProtocolError("prefill may only run once")
+        cfg = self.config
+        prompt = [int(t) for t in prompt]
+        if not prompt:
+            raise ValueError("prompt must be nonempty")
+        if len(prompt) > cfg.max_len:
+            raise ValueError("prompt longer than the configured max length")
+        n = len(prompt)
+        x = self.emb[prompt].clone()
+        mask = torch.tril(torch.ones((n, n), dtype=torch.bool, device=self.dev))
+        scale = np.float32(cfg.head_dim ** -0.5)
+        for layer, lw in enumerate(self.lw):
+            q, k, v = self._qkv(lw, x, range(n))
+            self.cache.prefill(layer, k[None], v[None])  # Alg. 1: slow tier + bulk quantization
+            # full-precision causal attention over the local prompt KV (engine.py:236-238)
+            qf, kf, vf = q.float(), k.float(), v.float()
+            outs = []
+            for hq in range(cfg.q_heads):
+                hk = hq // (cfg.q_heads // cfg.kv_heads)
+                s = (qf[:, hq, :] @ kf[:, hk, :].T) * float(scale)
+                s = torch.where(mask, s, torch.tensor(-math.inf, device=self.dev))
+                a = torch.softmax(s, dim=-1)
+                outs.append(a @ vf[:, hk, :])
+            att = torch.cat(outs, dim=1).to(torch.bfloat16).float()
+            x = self._ffn(lw, x + att @ lw["wo"])
+        self._pos = n
+        self._verified = int(torch.argmax(self._logits(x[-1:])[0]))
+        self._phase = "prefilled"
+        return self._verified
+
+    def _ticket_bytes(self, layer: int) -> tuple[int, int]:
+        _, newc = self.layer_dec.ticket(layer)
+        new = int(newc.sum().item())
+        return self.cache.row_bytes(new), new
+
+    def predecode(self) -> int:
+        import torch
+        if self._phase != "prefilled":
+            raise ProtocolError("predecode requires a completed prefill")
+        p = self._pos
+        x = self.emb[[self._verified]].clone()
+        for layer, lw in enumerate(self.lw):
+            q, k, v = self._qkv(lw, x, [p])
+            out = self.layer_dec.predecode_layer(layer, q[None], k[None], v[None])
+            nbytes, new = self._ticket_bytes(layer)
+            self.predecode_bytes += nbytes
+            self.predecode_new_pins += new
+            self._charge(0, nbytes)
+            x = self._ffn(lw, x + out[0].reshape(1, -1).float() @ lw["wo"])
+        self._speculative = int(torch.argmax(self._logits(x)[0]))
+        self._phase = "decoding"
+        self._step = 1
+        return self._speculative
+
+    def decode_step(self):
+        import torch
+        if self._phase != "decoding":
+            raise ProtocolError("decode_step requires predecode first")
+        p = self._pos
+        x = self.emb[[self._verified, self._speculative]].clone()
+        pin_mass, bytes_fetched, new_pins = [], 0, 0
+        for layer, lw in enumerate(self.lw):
+            q, k, v = self._qkv(lw, x, (p, p + 1))
+            res = self.layer_dec.decode_layer(layer, self._step, q[None], k[None], v[None])
+            pin_mass.append(res.pinned_mass[0].double().cpu().numpy())
+            nbytes, new = self._ticket_bytes(layer)
+            bytes_fetched += nbytes
+            new_pins += new
+            self._charge(self._step, nbytes)
+            x = self._ffn(lw, x + res.out[0].reshape(2, -1).float() @ lw["wo"])
+        logits = self._logits(x)
+        verified_next = int(torch.argmax(logits[0]))
+        speculative_next = int(torch.argmax(logits[1]))
+        metrics = StepMetrics(step=self._step, token=verified_next,
+                              speculative_hit=bool(verified_next == self._speculative),
+                              pinned_mass=float(np.mean(np.concatenate(pin_mass))),
+                              bytes_fetched=bytes_fetched, new_pins=new_pins)
+        self.last_logits = logits.cpu().numpy()
+        self._verified, self._speculative = verified_next, speculative_next
+        self._pos = p + 1
+        self._step += 1
+        return verified_next, metrics
+
+    # -- logical clock (transfer.py:90-112), the reference's report model --------------
+    def _charge(self, step: int, nbytes: int) -> None:
+        if nbytes > 0:
+            self._step_seconds[step] = self._step_seconds.get(step, 0.0) + transfer_time(
+                nbytes, self.channel_model, contiguous=False)
+
+    def step_transfer_seconds(self, step: int) -> float:
+        return self._step_seconds.get(step, 0.0)
+
+    def end_step(self, step: int, compute_s: float) -> float:
+        overlapped = step_latency(compute_s, self.step_transfer_seconds(step), overlapped=True)
+        self.clock += overlapped
+        return overlapped
+
+
+def generate(config, weights, prompt, steps: int, budget: CacheBudget,
+             channel_model: ChannelModel | None = None, mode: str = "sim",
+             compute_time_per_step: float = 0.0, prefill_time: float = 0.0,
+             device: int = 0) -> GenerateResult:
+    """engine.py:342-386 on the device."""
+    if steps < 1:
+        raise ValueError("steps must be >= 1")
+    dec = DeviceSpeculativeDecoder(config, weights, budget, channel_model, mode,
+                                   compute_time_per_step, prefill_time, device)
+    try:
+        tokens = [dec.prefill(prompt)]
+        dec.predecode()
+        compute_s = compute_time_per_step
+        pre_t = dec.step_transfer_seconds(0)
+        rows = [{"step": 0, "compute_s": compute_s, "transfer_s": pre_t,
+                 "overlapped_s": dec.end_step(0, compute_s),
+                 "serialized_s": step_latency(compute_s, pre_t, overlapped=False),
+                 "bytes": dec.predecode_bytes, "new_pins": dec.predecode_new_pins}]
+        logits, metrics = [], []
+        for _ in range(steps):
+            step_idx = dec._step
+            token, m = dec.decode_step()
+            tokens.append(token)
+            logits.append(dec.last_logits[0])
+            metrics.append(m)
+            t = dec.step_transfer_seconds(step_idx)
+            rows.append({"step": step_idx, "compute_s": compute_s, "transfer_s": t,
+                         "overlapped_s": dec.end_step(step_idx, compute_s),
+                         "serialized_s": step_latency(compute_s, t, overlapped=False),
+                         "bytes": m.bytes_fetched, "new_pins": m.new_pins})
+        return GenerateResult(tokens=tokens, logits=logits, metrics=metrics, latency_rows=rows,
+                              prefill_seconds=prefill_time, total_seconds=prefill_time + dec.clock,
+                              decoder=dec)
+    finally:
+        dec.close()

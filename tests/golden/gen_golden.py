@@ -224,6 +224,53 @@ def gen_decode(tag, bits, Hq, H, d, g, r, k, n0, steps, seed, tau=1.0):
     np.savez_compressed(os.path.join(HERE, f"decode_{tag}.npz"), **rec)
 
 
+def gen_adapter(tag, bits, g, r, k, L, prompt_len, steps, seed):
+    """Reference generate() (engine.py:342-386) with the hot-path boundary in
+    bf16: q/k/v rounded after _qkv, attention outputs rounded after _attend --
+    exactly what the device path receives and returns."""
+    from speckv.model import init_decoder
+    from speckv import engine as E
+    cfg = DecoderConfig(seed=seed)
+    w = init_decoder(cfg)
+    orig_qkv, orig_attend = E._qkv, E._attend
+
+    def qkv16(c, lw, x, positions):
+        q, k_, v = orig_qkv(c, lw, x, positions)
+        return bf16_round(q), bf16_round(k_), bf16_round(v)
+
+    def attend16(c, q, keys, vals, mask):
+        out, probs = orig_attend(c, q, keys, vals, mask)
+        return bf16_round(out), probs
+
+    E._qkv, E._attend = qkv16, attend16
+    try:
+        prompt = [int(t) for t in np.random.default_rng(seed + 100).integers(0, cfg.vocab, prompt_len)]
+        budget = CacheBudget(bits=bits, group_size=g, residual=r, prefetch_k=k, context_length=L)
+        res = E.generate(cfg, w, prompt, steps, budget, ChannelModel(bandwidth=1e6),
+                         compute_time_per_step=1e-3)
+        base_tokens, base_logits, _ = E.FullCacheDecoder(cfg, w).generate(prompt, steps)
+    finally:
+        E._qkv, E._attend = orig_qkv, orig_attend
+    rec = {"seed": np.int64(seed), "bits": np.int64(bits), "g": np.int64(g), "r": np.int64(r),
+           "k": np.int64(k), "L": np.int64(L), "prompt": np.asarray(prompt, np.int64),
+           "steps": np.int64(steps), "tokens": np.asarray(res.tokens, np.int64),
+           "logits": np.stack(res.logits), "base_tokens": np.asarray(base_tokens, np.int64),
+           "pinned_mass": np.asarray([m.pinned_mass for m in res.metrics]),
+           "bytes": np.asarray([m.bytes_fetched for m in res.metrics], np.int64),
+           "new_pins": np.asarray([m.new_pins for m in res.metrics], np.int64),
+           "hit": np.asarray([m.speculative_hit for m in res.metrics]),
+           "overlapped": np.asarray([r_["overlapped_s"] for r_ in res.latency_rows]),
+           "total_seconds": np.float64(res.total_seconds),
+           "w_embedding": w.embedding, "w_final_norm": w.final_norm, "w_head": w.head}
+    for i, lw in enumerate(w.layers):
+        for name in ("wq", "wk", "wv", "wo", "attn_norm", "ffn_norm", "w1", "w2"):
+            rec[f"w_{i}_{name}"] = getattr(lw, name)
+    for name in ("layers", "q_heads", "kv_heads", "head_dim", "vocab", "hidden", "ffn", "max_len"):
+        rec[f"cfg_{name}"] = np.int64(getattr(cfg, name))
+    rec["cfg_rope_base"] = np.float64(cfg.rope_base)
+    np.savez_compressed(os.path.join(HERE, f"adapter_{tag}.npz"), **rec)
+
+
 if __name__ == "__main__":
     gen_quant_groups()
     gen_cache("b2_d128", 2, 2, 128, 32, 32, 8, 200, [0, 5, 37, 100], seed=1)
@@ -236,4 +283,7 @@ if __name__ == "__main__":
     gen_decode("gqa_b1", 1, 8, 2, 128, 32, 32, 16, 300, 4, seed=8, tau=3.0)
     gen_decode("mha_b16", 16, 4, 4, 128, 32, 32, 16, 200, 3, seed=9)
     gen_decode("gqa4_b2", 2, 8, 2, 128, 32, 64, 32, 700, 5, seed=10)
+    gen_adapter("b2", 2, 4, 4, 4, 4096, 12, 10, seed=3)
+    gen_adapter("b1", 1, 4, 4, 4, 4096, 20, 10, seed=4)
+    gen_adapter("b16_exact", 16, 4, 8, 1024, 1024, 32, 16, seed=5)
     print("golden fixtures written to", HERE)
