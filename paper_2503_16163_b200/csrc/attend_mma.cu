@@ -176,7 +176,8 @@ struct ExactSmem {
 
 template <int BITS, int NR>
 constexpr size_t fast_smem_bytes() {
-  size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps, b = sizeof(MergeSmem<NR>), c = sizeof(ExactSmem<NR>);
+  size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps + (NR > 2 ? NR * 32 * 16 : 0), b = sizeof(MergeSmem<NR>),
+         c = sizeof(ExactSmem<NR>);
   return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 
@@ -402,18 +403,28 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
   // ---- per-lane constants ---------------------------------------------------------------
   // key-B role: lane (ks = lane&7, tk = lane>>3) owns channels 32tk + ks + 8m, m = 0..3
   const int kks = lane & 7, ktk = lane >> 3;
-  float Qr[NR][4];
+  constexpr bool QREG = NR <= 2;  // wide GQA rows keep the query slice in shared memory
+  float Qr[QREG ? NR : 1][4];
+  float4* Qs = reinterpret_cast<float4*>(smem_raw + kWarps * sizeof(WarpSmem<BITS, NR>));  // [NR][32]
   float qabs = 0.f;
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
     const int r = j / G.G, g2 = j - r * G.G;
     const __nv_bfloat16* qp = a.q + (((size_t)b * a.rows + r) * G.Hq + h * G.G + g2) * 128;
+    float qv[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-      Qr[j][m] = __bfloat162float(qp[32 * ktk + kks + 8 * m]) * a.sm_scale_log2;
-      qabs = fmaxf(qabs, fabsf(Qr[j][m]));
+      qv[m] = __bfloat162float(qp[32 * ktk + kks + 8 * m]) * a.sm_scale_log2;
+      qabs = fmaxf(qabs, fabsf(qv[m]));
+    }
+    if (QREG) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) Qr[QREG ? j : 0][m] = qv[m];
+    } else if (warp == 0) {
+      Qs[j * 32 + lane] = make_float4(qv[0], qv[1], qv[2], qv[3]);
     }
   }
+  if (!QREG) __syncthreads();
 #pragma unroll
   for (int o = 16; o; o >>= 1) qabs = fmaxf(qabs, __shfl_xor_sync(0xffffffffu, qabs, o));
   const float rk = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 2 + 0]) * cs;
@@ -487,9 +498,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
       }
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        const float w0 = Qr[j][0] * s4[0], w1 = Qr[j][1] * s4[1], w2 = Qr[j][2] * s4[2],
-                    w3 = Qr[j][3] * s4[3];
-        Cp[j] = fmaf(Qr[j][0], z4[0], fmaf(Qr[j][1], z4[1], fmaf(Qr[j][2], z4[2], Qr[j][3] * z4[3])));
+        float q0, q1, q2, q3;
+        if (QREG) {
+          q0 = Qr[QREG ? j : 0][0];
+          q1 = Qr[QREG ? j : 0][1];
+          q2 = Qr[QREG ? j : 0][2];
+          q3 = Qr[QREG ? j : 0][3];
+        } else {
+          const float4 qq = Qs[j * 32 + lane];
+          q0 = qq.x;
+          q1 = qq.y;
+          q2 = qq.z;
+          q3 = qq.w;
+        }
+        const float w0 = q0 * s4[0], w1 = q1 * s4[1], w2 = q2 * s4[2], w3 = q3 * s4[3];
+        Cp[j] = fmaf(q0, z4[0], fmaf(q1, z4[1], fmaf(q2, z4[2], q3 * z4[3])));
         uint4 frag;  // {b0hi, b1hi, b0lo, b1lo} of row j for fragment lane (j, tk)
         if (BITS == 2) {  // b0 = (m0, m1), b1 = (m2, m3)
           split2(w0, w1, frag.x, frag.z);
@@ -500,21 +523,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         }
         ws.bk[kks][(4 * j + ktk) ^ kks] = frag;
       }
-      if (NR == 2) {
-        // two-row reduce-scatter: after the first exchange lanes with bit4 == j
-        // carry row j; four more butterflies finish both rows (6 SHFL, not 10)
-        const bool hi16 = lane & 16;
-        float mine = hi16 ? Cp[1] : Cp[0];
-        const float other = hi16 ? Cp[0] : Cp[1];
-        mine += __shfl_xor_sync(0xffffffffu, other, 16);
+      // reduce-scatter of the NR per-lane partials: after log2(NR) halving steps a
+      // lane holds one row, r = lane >> (5 - log2 NR); the remaining butterflies
+      // finish the sum (NR=8: 9 SHFL instead of 40)
+      constexpr int LG = NR == 1 ? 0 : NR == 2 ? 1 : NR == 4 ? 2 : 3;
+      float v[NR];
 #pragma unroll
-        for (int o = 8; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-        Cp[0] = __shfl_sync(0xffffffffu, mine, 0);
-        Cp[1] = __shfl_sync(0xffffffffu, mine, 16);
-      } else {
+      for (int j = 0; j < NR; ++j) v[j] = Cp[j];
 #pragma unroll
-        for (int j = 0; j < NR; ++j) Cp[j] = warp_sum_all(Cp[j]);
+      for (int st2 = 0; st2 < LG; ++st2) {
+        const int o = 16 >> st2, half = NR >> (st2 + 1);
+        const bool up = lane & o;
+#pragma unroll
+        for (int i2 = 0; i2 < half; ++i2) {
+          const float keep = up ? v[i2 + half] : v[i2], send = up ? v[i2] : v[i2 + half];
+          v[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
       }
+#pragma unroll
+      for (int o = 16 >> LG; o; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+      Cp[0] = v[0];  // row (lane >> (5 - LG)) of this lane
     }
     // key codes of this lane's tokens T0 = 16mt + gq, T1 = T0 + 8
     uint32_t kw[2][2 * BITS];
@@ -584,12 +612,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
 
     // ---- epilogue: log2 scores, mask, spill, online softmax ----------------------------
     float cr[RPL];
+    {
+      constexpr int LG = NR == 1 ? 0 : NR == 2 ? 1 : NR == 4 ? 2 : 3;
 #pragma unroll
-    for (int e = 0; e < RPL; ++e) {
-      cr[e] = 0.f;
-#pragma unroll
-      for (int j = 0; j < NR; ++j)
-        if (j == jr[e]) cr[e] = Cp[j];
+      for (int e = 0; e < RPL; ++e)
+        cr[e] = __shfl_sync(0xffffffffu, Cp[0], (jr[e] & (NR - 1)) << (5 - LG));
     }
     // sc[mt][hf][e]: token T = 16mt + gq + 8hf, row jr[e]
     float sc[2][2][RPL];
