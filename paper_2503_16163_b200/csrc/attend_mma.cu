@@ -153,6 +153,7 @@ struct __align__(16) WarpSmem {
   uint4 bk[8][32];                                        // key B fragments, [ks][lane ^ ks]
   uint32_t stage[kStages][StageLayout<BITS>::words];      // TMA ring
   float P[NR][33];                                        // block probabilities [row][token]
+  float4 sz[64];                                          // value (s*2^-q, z) pairs, vparams order
   uint64_t bar[kStages];
 };
 
@@ -354,7 +355,7 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
 }
 
 template <int BITS, int NR>
-__global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
+__global__ void __launch_bounds__(kThreads, NR == 8 ? 1 : 2) k_attend_fast(AttnArgs a) {
   // PACK: score MMA columns n = 2*row + plane (hi/lo of each row side by side),
   //       one MMA per k-step and one score row per lane (row = lane & 3).
   // PG:   P.V columns n = group*NR + row, one B fragment for all value groups.
@@ -544,6 +545,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
       for (int o = 16 >> LG; o; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
       Cp[0] = v[0];  // row (lane >> (5 - LG)) of this lane
     }
+    // value params -> (s * 2^-(q+Ev), z) once per block: lane l decodes words 4l..4l+3
+    // (group l>>3, tq (l>>1)&3, ks l&1, slots 0..3; slot>>1 = khalf -> q = 2ks + khalf)
+    {
+      const uint4 vp4 = *reinterpret_cast<const uint4*>(S + SL::vp + 4 * lane);
+      const uint32_t vpw[4] = {vp4.x, vp4.y, vp4.z, vp4.w};
+      float o[8];
+#pragma unroll
+      for (int slot = 0; slot < 4; ++slot) {
+        const float lo = __uint_as_float(vpw[slot] << 16), hi = __uint_as_float(vpw[slot] & 0xFFFF0000u);
+        o[2 * slot] = (hi - lo) * vscale[2 * (lane & 1) + (slot >> 1)];
+        o[2 * slot + 1] = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
+      }
+      ws.sz[2 * lane] = make_float4(o[0], o[1], o[2], o[3]);
+      ws.sz[2 * lane + 1] = make_float4(o[4], o[5], o[6], o[7]);
+    }
     // key codes of this lane's tokens T0 = 16mt + gq, T1 = T0 + 8
     uint32_t kw[2][2 * BITS];
 #pragma unroll
@@ -709,36 +725,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     }
     __syncwarp();
 
-    // ---- value B fragments (f16 hi + lo: sum_t P*z and sum_t P*s*code may nearly cancel)
-    // PG: lane column n = gq -> (grp = gq / NR, row = gq % NR); else row = gq, per group
-    uint32_t vb[PG ? 1 : 4][2][4];  // [grp][ks] {b0hi, b1hi, b0lo, b1lo}
-#pragma unroll
-    for (int gi = 0; gi < (PG ? 1 : 4); ++gi) {
-      const int grp = PG ? ((gq / NR) & 3) : gi;
-      const int row = PG ? (gq % NR) : gq;
-      const bool live = PG ? (gq < 4 * NR) : (gq < NR);
-      const int prow = row < NR ? row : 0;
-      const uint4 v0 = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * grp + 8 * tq);
-      const uint4 v1 = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * grp + 8 * tq + 4);
-      const uint32_t vpw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};  // [ks][slot]
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        float x[4];
-#pragma unroll
-        for (int slot = 0; slot < 4; ++slot) {
-          const int khalf = slot >> 1;
-          const int t = 16 * ks + 2 * tq + (slot & 1) + 8 * khalf;
-          const uint32_t w = vpw[4 * ks + slot];
-          const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xFFFF0000u);
-          const float p = live ? ws.P[prow][t] : 0.f;
-          const float z = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
-          zacc[gi] = fmaf(p, z, zacc[gi]);
-          x[slot] = p * (hi - lo) * vscale[2 * ks + khalf];
-        }
-        split2(x[0], x[1], vb[gi][ks][0], vb[gi][ks][2]);
-        split2(x[2], x[3], vb[gi][ks][1], vb[gi][ks][3]);
-      }
-    }
     // value codes of this lane
     uint32_t vw[4 * BITS];
     {
@@ -756,7 +742,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
       }
     }
     __syncwarp();
-    // the stage is consumed: refill it with block it + kStages (async proxy after generic reads)
+    // the stage is consumed (codes in registers, params decoded to ws.sz): refill it
+    // with block it + kStages (async proxy after generic reads)
     if (lane == 0) {
       const int nblk = blk + kStages * kWarps;
       if (nblk < blk1) {
@@ -765,33 +752,61 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
       }
     }
 
-    // ---- P.V over 8 channel m-tiles x 2 token k-steps -------------------------------------
+    // ---- P.V: B fragments (f16 hi + lo: sum_t P*z and sum_t P*s*code may nearly
+    // cancel) and MMAs over 8 channel m-tiles x 2 token k-steps.  PG: one B for
+    // all groups (column n = gq -> (grp = gq / NR, row = gq % NR)); otherwise
+    // row = gq and group gi's fragment is built right before its two m-tiles.
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
+    for (int gi = 0; gi < (PG ? 1 : 4); ++gi) {
+      const int grp = PG ? ((gq / NR) & 3) : gi;
+      const int row = PG ? (gq % NR) : gq;
+      const bool live = PG ? (gq < 4 * NR) : (gq < NR);
+      const int prow = row < NR ? row : 0;
+      uint32_t vb[2][4];  // [ks] {b0hi, b1hi, b0lo, b1lo}
 #pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        uint32_t a0, a1, a2, a3;
-        const int q0 = 2 * ks, q1 = 2 * ks + 1;
-        if (BITS == 2) {
-          const uint32_t W = vw[mt % (4 * BITS)], W8 = W >> 8;
-          const uint32_t m0 = (3u << (2 * q0)) | (3u << (16 + 2 * q0));
-          const uint32_t m1 = (3u << (2 * q1)) | (3u << (16 + 2 * q1));
-          a0 = W & m0;
-          a1 = W8 & m0;
-          a2 = W & m1;
-          a3 = W8 & m1;
-        } else {
-          const uint32_t W = vw[(mt >> 1) % (4 * BITS)] >> (8 * (mt & 1)), W4 = W >> 4;
-          const uint32_t m0 = (1u << q0) | (1u << (16 + q0));
-          const uint32_t m1 = (1u << q1) | (1u << (16 + q1));
-          a0 = W & m0;
-          a1 = W4 & m0;
-          a2 = W & m1;
-          a3 = W4 & m1;
+      for (int ks = 0; ks < 2; ++ks) {
+        // (s', z) of tokens 16ks + 2tq + {0,1,8,9} of group grp: words 32grp + 8tq + 4ks + slot
+        const float4 sz0 = ws.sz[16 * grp + 4 * tq + 2 * ks];
+        const float4 sz1 = ws.sz[16 * grp + 4 * tq + 2 * ks + 1];
+        const float spr4[4] = {sz0.x, sz0.z, sz1.x, sz1.z}, zz4[4] = {sz0.y, sz0.w, sz1.y, sz1.w};
+        float x[4];
+#pragma unroll
+        for (int slot = 0; slot < 4; ++slot) {
+          const int khalf = slot >> 1;
+          const int t = 16 * ks + 2 * tq + (slot & 1) + 8 * khalf;
+          const float p = live ? ws.P[prow][t] : 0.f;
+          zacc[gi] = fmaf(p, zz4[slot], zacc[gi]);
+          x[slot] = p * spr4[slot];
         }
-        const int gi = PG ? 0 : (mt >> 1);
-        mma16816(dv[mt], a0, a1, a2, a3, vb[gi][ks][0], vb[gi][ks][1]);
-        mma16816(dv[mt], a0, a1, a2, a3, vb[gi][ks][2], vb[gi][ks][3]);
+        split2(x[0], x[1], vb[ks][0], vb[ks][2]);
+        split2(x[2], x[3], vb[ks][1], vb[ks][3]);
+      }
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+#pragma unroll
+        for (int mt = PG ? 0 : 2 * gi; mt < (PG ? 8 : 2 * gi + 2); ++mt) {
+          uint32_t a0, a1, a2, a3;
+          const int q0 = 2 * ks, q1 = 2 * ks + 1;
+          if (BITS == 2) {
+            const uint32_t W = vw[mt % (4 * BITS)], W8 = W >> 8;
+            const uint32_t m0 = (3u << (2 * q0)) | (3u << (16 + 2 * q0));
+            const uint32_t m1 = (3u << (2 * q1)) | (3u << (16 + 2 * q1));
+            a0 = W & m0;
+            a1 = W8 & m0;
+            a2 = W & m1;
+            a3 = W8 & m1;
+          } else {
+            const uint32_t W = vw[(mt >> 1) % (4 * BITS)] >> (8 * (mt & 1)), W4 = W >> 4;
+            const uint32_t m0 = (1u << q0) | (1u << (16 + q0));
+            const uint32_t m1 = (1u << q1) | (1u << (16 + q1));
+            a0 = W & m0;
+            a1 = W4 & m0;
+            a2 = W & m1;
+            a3 = W4 & m1;
+          }
+          mma16816(dv[mt], a0, a1, a2, a3, vb[ks][0], vb[ks][1]);
+          mma16816(dv[mt], a0, a1, a2, a3, vb[ks][2], vb[ks][3]);
+        }
       }
     }
     bm = nbm;
