@@ -13,7 +13,7 @@ import re
 from .transfer import ProtocolError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspecache.so")
+LIB_PATH = os.environ.get("SPC_LIB_PATH") or os.path.join(_HERE, "libspecache.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "specache.h")
 
 SPC_OK, SPC_EINVAL, SPC_EPROTO, SPC_ENOMEM, SPC_ECUDA = 0, -22, -71, -12, -5

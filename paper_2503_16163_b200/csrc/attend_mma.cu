@@ -150,7 +150,7 @@ struct StageLayout {
 
 template <int BITS, int NR>
 struct __align__(16) WarpSmem {
-  uint4 bk[8][32];                                        // key B fragments, [ks][lane ^ ks]
+  uint4 bk[8][4 * NR];  // key B fragments {b0hi, b1hi, b0lo, b1lo} of lane (row j, t'), [ks][4j + (t' ^ (ks&3))]
   uint32_t stage[kStages][StageLayout<BITS>::words];      // TMA ring
   float P[NR][33];                                        // block probabilities [row][token]
   float4 sz[64];                                          // value (s*2^-q, z) pairs, vparams order
@@ -355,7 +355,7 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
 }
 
 template <int BITS, int NR>
-__global__ void __launch_bounds__(kThreads, NR == 8 ? 1 : 2) k_attend_fast(AttnArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
   // PACK: score MMA columns n = 2*row + plane (hi/lo of each row side by side),
   //       one MMA per k-step and one score row per lane (row = lane & 3).
   // PG:   P.V columns n = group*NR + row, one B fragment for all value groups.
@@ -450,10 +450,6 @@ __global__ void __launch_bounds__(kThreads, NR == 8 ? 1 : 2) k_attend_fast(AttnA
                  ? a.spill + ((size_t)b * G.Hq + h * G.G + (jr[e] - agg_j0)) * G.L : nullptr;
   }
 
-  for (int i = lane; i < 8 * 32; i += 32) {  // unused rows of the key-B fragments stay 0
-    const int ks = i >> 5, l = i & 31;
-    if ((l >> 2) >= NR) ws.bk[ks][l ^ ks] = make_uint4(0, 0, 0, 0);
-  }
 
   float m_run[RPL], l_run[RPL];
 #pragma unroll
@@ -522,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, NR == 8 ? 1 : 2) k_attend_fast(AttnA
           split2(w0, w2, frag.x, frag.z);
           split2(w1, w3, frag.y, frag.w);
         }
-        ws.bk[kks][(4 * j + ktk) ^ kks] = frag;
+        ws.bk[kks][4 * j + (ktk ^ (kks & 3))] = frag;
       }
       // reduce-scatter of the NR per-lane partials: after log2(NR) halving steps a
       // lane holds one row, r = lane >> (5 - log2 NR); the remaining butterflies
@@ -587,12 +583,13 @@ __global__ void __launch_bounds__(kThreads, NR == 8 ? 1 : 2) k_attend_fast(AttnA
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
       uint32_t b0, b1, b2 = 0, b3 = 0;
-      if (PACK) {  // column n = gq = 2*row + plane
-        const uint2 bb = reinterpret_cast<const uint2*>(&ws.bk[ks][(4 * (gq >> 1) + tq) ^ ks])[gq & 1];
+      if (PACK) {  // column n = gq = 2*row + plane; rows >= NR are zero columns
+        uint2 bb = make_uint2(0, 0);
+        if ((gq >> 1) < NR) bb = reinterpret_cast<const uint2*>(&ws.bk[ks][4 * (gq >> 1) + (tq ^ (ks & 3))])[gq & 1];
         b0 = bb.x;
         b1 = bb.y;
       } else {
-        const uint4 bb = ws.bk[ks][lane ^ ks];
+        const uint4 bb = ws.bk[ks][4 * gq + (tq ^ (ks & 3))];
         b0 = bb.x;
         b1 = bb.y;
         b2 = bb.z;
@@ -907,6 +904,8 @@ __global__ void __launch_bounds__(kThreads, NR == 8 ? 1 : 2) k_attend_fast(AttnA
 template <int BITS, int NR>
 void launch_fast_t(const AttnArgs& a, cudaStream_t st) {
   constexpr size_t smem = fast_smem_bytes<BITS, NR>();
+  // two CTAs per SM (228 KB, 1 KB reserved per CTA) is the design point
+  static_assert((BITS == 2 && NR == 8) || smem <= 113 * 1024, "K2 shared memory exceeds 2 CTAs/SM");
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_attend_fast<BITS, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
