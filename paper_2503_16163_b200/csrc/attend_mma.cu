@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     }
     // value params -> (s * 2^-(q+Ev), z) once per block: lane l decodes words 4l..4l+3
     // (group l>>3, tq (l>>1)&3, ks l&1, slots 0..3; slot>>1 = khalf -> q = 2ks + khalf)
-    {
+    if constexpr (PG) {
       const uint4 vp4 = *reinterpret_cast<const uint4*>(S + SL::vp + 4 * lane);
       const uint32_t vpw[4] = {vp4.x, vp4.y, vp4.z, vp4.w};
       float o[8];
@@ -722,6 +722,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
     }
     __syncwarp();
 
+    if constexpr (PG) {
     // value codes of this lane
     uint32_t vw[4 * BITS];
     {
@@ -805,6 +806,93 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
           mma16816(dv[mt], a0, a1, a2, a3, vb[ks][2], vb[ks][3]);
         }
       }
+    }
+    } else {
+    // ---- value B fragments (f16 hi + lo: sum_t P*z and sum_t P*s*code may nearly cancel)
+    // PG: lane column n = gq -> (grp = gq / NR, row = gq % NR); else row = gq, per group
+    uint32_t vb[PG ? 1 : 4][2][4];  // [grp][ks] {b0hi, b1hi, b0lo, b1lo}
+#pragma unroll
+    for (int gi = 0; gi < (PG ? 1 : 4); ++gi) {
+      const int grp = PG ? ((gq / NR) & 3) : gi;
+      const int row = PG ? (gq % NR) : gq;
+      const bool live = PG ? (gq < 4 * NR) : (gq < NR);
+      const int prow = row < NR ? row : 0;
+      const uint4 v0 = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * grp + 8 * tq);
+      const uint4 v1 = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * grp + 8 * tq + 4);
+      const uint32_t vpw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};  // [ks][slot]
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        float x[4];
+#pragma unroll
+        for (int slot = 0; slot < 4; ++slot) {
+          const int khalf = slot >> 1;
+          const int t = 16 * ks + 2 * tq + (slot & 1) + 8 * khalf;
+          const uint32_t w = vpw[4 * ks + slot];
+          const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xFFFF0000u);
+          const float p = live ? ws.P[prow][t] : 0.f;
+          const float z = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
+          zacc[gi] = fmaf(p, z, zacc[gi]);
+          x[slot] = p * (hi - lo) * vscale[2 * ks + khalf];
+        }
+        split2(x[0], x[1], vb[gi][ks][0], vb[gi][ks][2]);
+        split2(x[2], x[3], vb[gi][ks][1], vb[gi][ks][3]);
+      }
+    }
+    // value codes of this lane
+    uint32_t vw[4 * BITS];
+    {
+      const uint4 w0 = *reinterpret_cast<const uint4*>(S + SL::vc + lane * 4);
+      vw[0] = w0.x;
+      vw[1] = w0.y;
+      vw[2] = w0.z;
+      vw[3] = w0.w;
+      if (BITS == 2) {
+        const uint4 w1 = *reinterpret_cast<const uint4*>(S + SL::vc + 128 + lane * 4);
+        vw[4 % (4 * BITS)] = w1.x;
+        vw[5 % (4 * BITS)] = w1.y;
+        vw[6 % (4 * BITS)] = w1.z;
+        vw[7 % (4 * BITS)] = w1.w;
+      }
+    }
+    __syncwarp();
+    // the stage is consumed: refill it with block it + kStages (async proxy after generic reads)
+    if (lane == 0) {
+      const int nblk = blk + kStages * kWarps;
+      if (nblk < blk1) {
+        fence_proxy_async();
+        issue(nblk, st);
+      }
+    }
+
+    // ---- P.V over 8 channel m-tiles x 2 token k-steps -------------------------------------
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t a0, a1, a2, a3;
+        const int q0 = 2 * ks, q1 = 2 * ks + 1;
+        if (BITS == 2) {
+          const uint32_t W = vw[mt % (4 * BITS)], W8 = W >> 8;
+          const uint32_t m0 = (3u << (2 * q0)) | (3u << (16 + 2 * q0));
+          const uint32_t m1 = (3u << (2 * q1)) | (3u << (16 + 2 * q1));
+          a0 = W & m0;
+          a1 = W8 & m0;
+          a2 = W & m1;
+          a3 = W8 & m1;
+        } else {
+          const uint32_t W = vw[(mt >> 1) % (4 * BITS)] >> (8 * (mt & 1)), W4 = W >> 4;
+          const uint32_t m0 = (1u << q0) | (1u << (16 + q0));
+          const uint32_t m1 = (1u << q1) | (1u << (16 + q1));
+          a0 = W & m0;
+          a1 = W4 & m0;
+          a2 = W & m1;
+          a3 = W4 & m1;
+        }
+        const int gi = PG ? 0 : (mt >> 1);
+        mma16816(dv[mt], a0, a1, a2, a3, vb[gi][ks][0], vb[gi][ks][1]);
+        mma16816(dv[mt], a0, a1, a2, a3, vb[gi][ks][2], vb[gi][ks][3]);
+      }
+    }
     }
     bm = nbm;
     if (++st == kStages) {
