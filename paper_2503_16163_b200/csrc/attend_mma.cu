@@ -208,11 +208,15 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
     Qr[j][3] = __high2float(q23) * a.sm_scale_log2;
   }
   const int32_t* pp = B.pin_pos + ((size_t)b * G.U + unit) * G.k;
-  if (tid == 0) {
+  if (warp == 0) {  // ballot compaction of the occupied slots, in slot order
     int cnt = 0;
-    for (int s = 0; s < G.k; ++s)
-      if (pp[s] >= 0) ex.slots[cnt++] = s;
-    ex.npin = cnt;
+    for (int s0 = 0; s0 < G.k; s0 += 32) {
+      const bool occ = s0 + lane < G.k && pp[s0 + lane] >= 0;
+      const unsigned m = __ballot_sync(0xffffffffu, occ);
+      if (occ) ex.slots[cnt + __popc(m & ((1u << lane) - 1u))] = s0 + lane;
+      cnt += __popc(m);
+    }
+    if (lane == 0) ex.npin = cnt;
   }
   if (tid < NR) {
     ex.m[tid] = -CUDART_INF_F;
@@ -254,24 +258,44 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
     int cend = min(total, c0 + CH);
     if (c0 < npin) cend = min(cend, npin);
     const int count = cend - c0;
-    for (int it = warp; it < count; it += kWarps) {
-      const __nv_bfloat16 *kr, *vr;
-      int pos;
-      bool spec;
-      row_ptr(c0 + it, kr, vr, pos, spec);
-      const uint2 w = *reinterpret_cast<const uint2*>(kr + 4 * lane);
-      const __nv_bfloat162 k01 = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
-      const __nv_bfloat162 k23 = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
-      const float k0 = __low2float(k01), k1 = __high2float(k01), k2 = __low2float(k23), k3 = __high2float(k23);
+    // scores: each warp keeps kRows rows in flight (independent 8-byte loads per
+    // lane), then reduces them over the warp
+    constexpr int kRows = 4;
+    for (int it0 = warp; it0 < count; it0 += kWarps * kRows) {
+      float k4[kRows][4];
+      int posr[kRows];
+      bool specr[kRows];
 #pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        float s = fmaf(Qr[j][0], k0, fmaf(Qr[j][1], k1, fmaf(Qr[j][2], k2, Qr[j][3] * k3)));
-        s = warp_sum_all(s);
-        if (lane == j) {
-          const bool m = spec && j < G.G;  // row 0 never sees the speculative column
-          ex.sc[j][it] = m ? -CUDART_INF_F : s;
-          if (pos >= 0 && j >= agg_j0 && j < agg_j0 + G.G)
-            a.spill[((size_t)b * G.Hq + h * G.G + (j - agg_j0)) * G.L + pos] = s;
+      for (int u = 0; u < kRows; ++u) {
+        const int it = it0 + u * kWarps;
+        k4[u][0] = k4[u][1] = k4[u][2] = k4[u][3] = 0.f;
+        posr[u] = -1;
+        specr[u] = false;
+        if (it < count) {
+          const __nv_bfloat16 *kr, *vr;
+          row_ptr(c0 + it, kr, vr, posr[u], specr[u]);
+          const uint2 w = *reinterpret_cast<const uint2*>(kr + 4 * lane);
+          const __nv_bfloat162 k01 = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
+          const __nv_bfloat162 k23 = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
+          k4[u][0] = __low2float(k01);
+          k4[u][1] = __high2float(k01);
+          k4[u][2] = __low2float(k23);
+          k4[u][3] = __high2float(k23);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kRows; ++u) {
+        const int it = it0 + u * kWarps;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          float sv = fmaf(Qr[j][0], k4[u][0], fmaf(Qr[j][1], k4[u][1], fmaf(Qr[j][2], k4[u][2], Qr[j][3] * k4[u][3])));
+          sv = warp_sum_all(sv);
+          if (lane == j && it < count) {
+            const bool m = specr[u] && j < G.G;  // row 0 never sees the speculative column
+            ex.sc[j][it] = m ? -CUDART_INF_F : sv;
+            if (posr[u] >= 0 && j >= agg_j0 && j < agg_j0 + G.G)
+              a.spill[((size_t)b * G.Hq + h * G.G + (j - agg_j0)) * G.L + posr[u]] = sv;
+          }
         }
       }
     }
@@ -307,22 +331,39 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
       acc[j][2] *= f;
       acc[j][3] *= f;
     }
-    for (int it = warp; it < count; it += kWarps) {
-      const __nv_bfloat16 *kr, *vr;
-      int pos;
-      bool spec;
-      row_ptr(c0 + it, kr, vr, pos, spec);
-      const uint2 w = *reinterpret_cast<const uint2*>(vr + 4 * lane);
-      const __nv_bfloat162 v01 = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
-      const __nv_bfloat162 v23 = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
-      const float v0 = __low2float(v01), v1 = __high2float(v01), v2 = __low2float(v23), v3 = __high2float(v23);
+    for (int it0 = warp; it0 < count; it0 += kWarps * kRows) {
+      float v4[kRows][4];
 #pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        const float p = ex.sc[j][it];
-        acc[j][0] = fmaf(p, v0, acc[j][0]);
-        acc[j][1] = fmaf(p, v1, acc[j][1]);
-        acc[j][2] = fmaf(p, v2, acc[j][2]);
-        acc[j][3] = fmaf(p, v3, acc[j][3]);
+      for (int u = 0; u < kRows; ++u) {
+        const int it = it0 + u * kWarps;
+        v4[u][0] = v4[u][1] = v4[u][2] = v4[u][3] = 0.f;
+        if (it < count) {
+          const __nv_bfloat16 *kr, *vr;
+          int pos;
+          bool spec;
+          row_ptr(c0 + it, kr, vr, pos, spec);
+          const uint2 w = *reinterpret_cast<const uint2*>(vr + 4 * lane);
+          const __nv_bfloat162 v01 = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
+          const __nv_bfloat162 v23 = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
+          v4[u][0] = __low2float(v01);
+          v4[u][1] = __high2float(v01);
+          v4[u][2] = __low2float(v23);
+          v4[u][3] = __high2float(v23);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kRows; ++u) {
+        const int it = it0 + u * kWarps;
+        if (it < count) {
+#pragma unroll
+          for (int j = 0; j < NR; ++j) {
+            const float p = ex.sc[j][it];
+            acc[j][0] = fmaf(p, v4[u][0], acc[j][0]);
+            acc[j][1] = fmaf(p, v4[u][1], acc[j][1]);
+            acc[j][2] = fmaf(p, v4[u][2], acc[j][2]);
+            acc[j][3] = fmaf(p, v4[u][3], acc[j][3]);
+          }
+        }
       }
     }
     __syncthreads();
