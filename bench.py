@@ -368,6 +368,9 @@ def run_gpu_arm(args, cfg):
         torch.cuda.synchronize(device)
     elapsed_ms = ev0.elapsed_time(ev1)
     attn_ms, attn_n, sel_ms, sel_n, launches = profile(0)
+    wait_ms = lib.spc_profile_wait_ms(h)
+    pf_ms = lib.spc_profile_prefetch_ms(h)
+    pf_bytes = int(lib.spc_profile_prefetch_bytes(h))
     _, newc = dec.ticket(L // 2)
     npin = int((picked0 >= 0).sum().item()) // max(1, cfg["batch"])
     new_frac = float(newc.float().mean().item()) / max(1, cfg["topk"])
@@ -430,7 +433,7 @@ def run_gpu_arm(args, cfg):
                 traffic = tr["bytes_per_launch"]
     except (OSError, ValueError):
         pass
-    h2d_pf = new_frac * cfg["topk"] * cfg["batch"] * cfg["layers"] * cache.row_bytes(1)
+    h2d_pf = pf_bytes / K  # measured: new pins x row bytes, summed over the timed steps
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -446,8 +449,11 @@ def run_gpu_arm(args, cfg):
                      "kernel": "K2 attend (per layer launch, all sequences)",
                      "algorithmic_bytes_per_launch": ab["hbm"], "avg_launch_ms": attn_avg_ms,
                      "launches": attn_n, "kernel_share_of_step": attn_ms / max(1e-9, elapsed_ms)},
-        "prefetch": {"new_pin_fraction": new_frac, "h2d_bytes_per_step": h2d_pf,
-                     "copy_stream_ms_per_step": sel_ms / K, "h2d_gbs_if_serial": (h2d_pf / 1e9) / max(1e-9, sel_ms / K / 1e3)},
+        "prefetch": {"new_pin_fraction": h2d_pf / max(1, cfg["topk"] * cfg["batch"] * cfg["layers"] * cache.row_bytes(1)),
+                     "h2d_bytes_per_step": h2d_pf,
+                     "exposed_ms_per_step": wait_ms / K, "exposed_fraction": wait_ms / max(1e-9, elapsed_ms),
+                     "copy_stream_ms_per_step": sel_ms / K, "prefetch_kernel_ms_per_step": pf_ms / K,
+                     "h2d_gbs": (h2d_pf / 1e9) / max(1e-9, pf_ms / K / 1e3)},
         "e2e": {"value": tokens / e2e_s,
                 "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,

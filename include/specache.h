@@ -157,6 +157,13 @@ SPC_API int spc_slow_fetch(spc_cache* cache, int layer, int seq, const int32_t* 
  * recording on (enable=1) or off. */
 SPC_API int spc_profile(spc_cache* cache, int enable, double* attn_ms, int64_t* attn_launches,
                         double* sel_ms, int64_t* sel_launches, int64_t* launches);
+/* Exposed prefetch of the last spc_profile window: summed compute-stream time
+ * (ms) between reaching a decode layer and its ticket's prefetch event. */
+SPC_API double spc_profile_wait_ms(const spc_cache* cache);
+/* K5 (PCIe prefetch gather) kernel time of the last spc_profile window (ms). */
+SPC_API double spc_profile_prefetch_ms(const spc_cache* cache);
+/* Bytes the K5 gathers moved over PCIe in the last spc_profile window. */
+SPC_API int64_t spc_profile_prefetch_bytes(const spc_cache* cache);
 /* Device pointer + element count of the pin state of (layer): pin_pos int32
  * [batch][units][k] (-1 = empty slot). */
 SPC_API int spc_pin_state(spc_cache* cache, int layer, const int32_t** pin_pos);

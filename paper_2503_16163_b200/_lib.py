@@ -54,6 +54,9 @@ _SIGS = {
     "spc_export_packed": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "spc_slow_fetch": (_I, [_P, _I, _I, _P, _I, _P, _P]),
     "spc_pin_state": (_I, [_P, _I, ctypes.POINTER(_P)]),
+    "spc_profile_wait_ms": (ctypes.c_double, [_P]),
+    "spc_profile_prefetch_ms": (ctypes.c_double, [_P]),
+    "spc_profile_prefetch_bytes": (_I64, [_P]),
     "spc_profile": (_I, [_P, _I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
 }

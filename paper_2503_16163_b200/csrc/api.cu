@@ -63,13 +63,16 @@ struct spc_cache {
   cudaStream_t cstream(int layer) const { return (layer & 1) ? copy_stream2 : copy_stream; }
   float *part_o = nullptr, *part_ml = nullptr, *pin_ml = nullptr, *spill = nullptr, *mz = nullptr;
   int32_t* staging = nullptr;
+  unsigned long long* pf_rows = nullptr;
   int context_length = 0;
   // live profiling of the dominant kernel (K2) and the copy-stream work (K4+K5)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_attn, prof_sel;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_attn, prof_sel, prof_wait, prof_pf;
   int64_t launches = 0;
+  double last_wait_ms = 0, last_pf_ms = 0;
+  int64_t last_pf_rows = 0;
 };
 
 namespace {
@@ -213,7 +216,17 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
   launch_agg(a, cs);
   c->launches += a.f > 0;
   launch_topk(G, c->L[layer], a.f, cs);
+  cudaEvent_t q0 = nullptr, q1 = nullptr;
+  if (c->prof) {
+    q0 = prof_event(c);
+    q1 = prof_event(c);
+    CUDA_TRY(cudaEventRecord(q0, cs));
+  }
   launch_prefetch(G, c->L[layer], host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer), cs);
+  if (c->prof) {
+    CUDA_TRY(cudaEventRecord(q1, cs));
+    c->prof_pf.push_back({q0, q1});
+  }
   c->launches += 2;
   CUDA_TRY(cudaGetLastError());
   if (c->prof) {
@@ -341,6 +354,11 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
   if (rc == SPC_OK) rc = dalloc(c, (void**)&c->spill, (size_t)G.layers * b * G.Hq * (size_t)G.L * 4);
   if (rc == SPC_OK) rc = dalloc(c, (void**)&c->mz, (size_t)G.layers * b * G.Hq * 2 * 4);
   if (rc == SPC_OK) rc = dalloc(c, (void**)&c->staging, (size_t)G.k * 4);
+  if (rc == SPC_OK) rc = dalloc(c, (void**)&c->pf_rows, sizeof(unsigned long long));
+  if (rc == SPC_OK) {
+    cudaMemset(c->pf_rows, 0, sizeof(unsigned long long));
+    for (auto& B : c->L) B.pf_rows = c->pf_rows;
+  }
   if (rc == SPC_OK) {
     c->slab_elems = b * (size_t)G.L * H * G.d;
     c->host_bytes = 2 * c->slab_elems * G.host_layers * sizeof(__nv_bfloat16);
@@ -517,7 +535,17 @@ int spc_decode_layer(spc_cache* c, int layer, int step, const void* q, const voi
                                 std::to_string(layer));
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t w0 = nullptr, w1 = nullptr;
+  if (c->prof) {  // exposed prefetch: compute-stream time spent waiting on the ticket
+    w0 = prof_event(c);
+    w1 = prof_event(c);
+    CUDA_TRY(cudaEventRecord(w0, st));
+  }
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));  // await_layer
+  if (c->prof) {
+    CUDA_TRY(cudaEventRecord(w1, st));
+    c->prof_wait.push_back({w0, w1});
+  }
   c->ticket[layer] = -1;
   // persists row 0 only (engine.py:321; the speculative row is never persisted)
   int rc = run_layer(c, layer, 2, q, k_new, v_new, out, pinned_mass, st, true);
@@ -605,6 +633,24 @@ int spc_profile(spc_cache* c, int enable, double* attn_ms, int64_t* attn_launche
     CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
     s += ms;
   }
+  double w = 0;
+  for (auto& p : c->prof_wait) {
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
+    w += ms;
+  }
+  c->last_wait_ms = w;
+  double pf = 0;
+  for (auto& p : c->prof_pf) {
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
+    pf += ms;
+  }
+  c->last_pf_ms = pf;
+  unsigned long long rows = 0;
+  CUDA_TRY(cudaMemcpy(&rows, c->pf_rows, sizeof(rows), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemset(c->pf_rows, 0, sizeof(rows)));
+  c->last_pf_rows = (int64_t)rows;
   if (attn_ms) *attn_ms = a;
   if (attn_launches) *attn_launches = (int64_t)c->prof_attn.size();
   if (sel_ms) *sel_ms = s;
@@ -612,10 +658,19 @@ int spc_profile(spc_cache* c, int enable, double* attn_ms, int64_t* attn_launche
   if (launches) *launches = c->launches;
   c->prof_attn.clear();
   c->prof_sel.clear();
+  c->prof_wait.clear();
+  c->prof_pf.clear();
   c->ev_used = 0;
   c->launches = 0;
   c->prof = enable != 0;
   return SPC_OK;
+}
+
+double spc_profile_wait_ms(const spc_cache* c) { return c ? c->last_wait_ms : -1.0; }
+double spc_profile_prefetch_ms(const spc_cache* c) { return c ? c->last_pf_ms : -1.0; }
+int64_t spc_profile_prefetch_bytes(const spc_cache* c) {
+  // one new pin moves the K and V rows of the unit's heads (16-bit accounting, kvcache.py:148-150)
+  return c ? c->last_pf_rows * (int64_t)2 * c->G.Hu * c->G.d * 2 : -1;
 }
 
 int spc_pin_state(spc_cache* c, int layer, const int32_t** pin_pos) {

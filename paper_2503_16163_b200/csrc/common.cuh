@@ -63,6 +63,7 @@ struct LayerBufs {
   int32_t* fetch_slot; // [b][U][k]
   int32_t* fetch_pos;  // [b][U][k]
   uint32_t* rmax;      // [b][H][2] max group range (hi-lo) of keys / values, fp32 bits
+  unsigned long long* pf_rows;  // cache-wide count of prefetched (new) pin rows (profiling)
 };
 
 // ---- element offsets ---------------------------------------------------------

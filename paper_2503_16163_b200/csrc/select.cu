@@ -191,7 +191,10 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(Geo G, LayerBufs B, int f
     B.fetch_pos[bu * G.k + i] = p;
   }
   for (int i = tid; i < G.k; i += kTopkThreads) B.sel[bu * G.k + i] = i < K ? sel[i] : -1;
-  if (tid == 0) B.newcnt[bu] = nnew;
+  if (tid == 0) {
+    B.newcnt[bu] = nnew;
+    atomicAdd(B.pf_rows, (unsigned long long)nnew);
+  }
 }
 
 void launch_topk(const Geo& G, const LayerBufs& B, int f, cudaStream_t st) {
