@@ -244,12 +244,13 @@ void launch_set_pins(const Geo& G, const LayerBufs& B, int seq, int unit, const 
 }
 
 // K5: PCIe gather of the new pins (zero-copy loads from the pinned host tier).
-// A small grid (kPfCtas CTAs per (seq, unit)) keeps SM slots free for K2 while
+// A small grid (kPfCtas CTA per (seq, unit)): a resident prefetch CTA costs its SM
+// one K2 CTA slot (registers) for the whole PCIe-bound gather, so keep few, while
 // each thread keeps kPfUnroll independent 16-byte host loads in flight, enough
 // to cover PCIe latency at full link rate.  Rows of a unit's heads are
 // contiguous in the host tier ([pos][H][d]).
-constexpr int kPfCtas = 4;
-constexpr int kPfUnroll = 8;
+constexpr int kPfCtas = 1;
+constexpr int kPfUnroll = 16;
 
 __global__ void __launch_bounds__(256) k_prefetch(Geo G, LayerBufs B, const uint4* host_k,
                                                   const uint4* host_v, int seq0, int unit0, int one) {
