@@ -11,8 +11,13 @@ boundary is bf16: q/k/v enter the cache and the attention as bf16, attention
 outputs leave as bf16 (the C ABI contract).
 
 Same constructor arguments, phase rules (ProtocolError), StepMetrics and
-GenerateResult fields as the reference; the transfer-latency report rows use
-the reference's logical-clock model (transfer.py:58-112).
+GenerateResult fields as the reference.  The latency rows use the reference's
+logical-clock model (transfer.py:58-112) by default; clock="measured"
+replaces it with CUDA-event timings of each step on the device (SURVEY 8(f)
+row 3): overlapped_s = the step's device time on the compute stream (exposed
+prefetch waits included), transfer_s = the step's PCIe gather kernels,
+compute_s = overlapped_s minus the exposed waits, serialized_s = compute_s +
+transfer_s.
 """
 from __future__ import annotations
 
@@ -47,10 +52,15 @@ class DeviceSpeculativeDecoder:
 
     def __init__(self, config, weights, budget: CacheBudget, channel_model: ChannelModel | None = None,
                  mode: str = "sim", compute_time_per_step: float = 0.0, prefill_time: float = 0.0,
-                 device: int = 0):
+                 device: int = 0, clock: str = "logical"):
         import torch
         if mode not in ("sim", "thread"):
             raise ValueError("mode must be 'sim' or 'thread'")
+        if clock not in ("logical", "measured"):
+            raise ValueError("clock must be 'logical' or 'measured'")
+        self.clock_mode = clock
+        self._measured: dict[int, dict] = {}
+        self._ev = None
         torch.backends.cuda.matmul.allow_tf32 = False  # fp32 model math, as the reference
         self.config, self.budget = config, budget
         self.dev = f"cuda:{device}"
@@ -165,6 +175,7 @@ class DeviceSpeculativeDecoder:
         if self._phase != "prefilled":
             raise ProtocolError("predecode requires a completed prefill")
         p = self._pos
+        self._measure_begin()
         x = self.emb[[self._verified]].clone()
         for layer, lw in enumerate(self.lw):
             q, k, v = self._qkv(lw, x, [p])
@@ -175,6 +186,7 @@ class DeviceSpeculativeDecoder:
             self._charge(0, nbytes)
             x = self._ffn(lw, x + out[0].reshape(1, -1).float() @ lw["wo"])
         self._speculative = int(torch.argmax(self._logits(x)[0]))
+        self._measure_end(0)
         self._phase = "decoding"
         self._step = 1
         return self._speculative
@@ -184,6 +196,7 @@ class DeviceSpeculativeDecoder:
         if self._phase != "decoding":
             raise ProtocolError("decode_step requires predecode first")
         p = self._pos
+        self._measure_begin()
         x = self.emb[[self._verified, self._speculative]].clone()
         pin_mass, bytes_fetched, new_pins = [], 0, 0
         for layer, lw in enumerate(self.lw):
@@ -198,6 +211,7 @@ class DeviceSpeculativeDecoder:
         logits = self._logits(x)
         verified_next = int(torch.argmax(logits[0]))
         speculative_next = int(torch.argmax(logits[1]))
+        self._measure_end(self._step)
         metrics = StepMetrics(step=self._step, token=verified_next,
                               speculative_hit=bool(verified_next == self._speculative),
                               pinned_mass=float(np.mean(np.concatenate(pin_mass))),
@@ -215,6 +229,8 @@ class DeviceSpeculativeDecoder:
                 nbytes, self.channel_model, contiguous=False)
 
     def step_transfer_seconds(self, step: int) -> float:
+        if self.clock_mode == "measured":
+            return self._measured.get(step, {}).get("transfer_s", 0.0)
         return self._step_seconds.get(step, 0.0)
 
     def end_step(self, step: int, compute_s: float) -> float:
@@ -222,24 +238,53 @@ class DeviceSpeculativeDecoder:
         self.clock += overlapped
         return overlapped
 
+    # -- measured clock (CUDA events + the library's per-launch event pairs) -------------
+    def _measure_begin(self) -> None:
+        if self.clock_mode != "measured":
+            return
+        import torch
+        self.cache.profile(True)  # drain + reset, record events for this step
+        self._ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        self._ev[0].record()
+
+    def _measure_end(self, step: int) -> None:
+        if self.clock_mode != "measured":
+            return
+        self._ev[1].record()
+        prof = self.cache.profile(False)  # synchronizes the device
+        step_s = self._ev[0].elapsed_time(self._ev[1]) / 1e3
+        compute = max(0.0, step_s - prof["wait_ms"] / 1e3)
+        transfer = prof["prefetch_ms"] / 1e3
+        self._measured[step] = {"compute_s": compute, "transfer_s": transfer, "overlapped_s": step_s,
+                                "serialized_s": compute + transfer, "h2d_bytes": prof["prefetch_bytes"],
+                                "attn_s": prof["attn_ms"] / 1e3}
+
+    def latency_row(self, step: int, compute_s: float) -> dict:
+        """One report row's timing fields (engine.py:361-381), advancing the clock."""
+        if self.clock_mode == "measured":
+            m = self._measured[step]
+            self.clock += m["overlapped_s"]
+            return {"compute_s": m["compute_s"], "transfer_s": m["transfer_s"],
+                    "overlapped_s": m["overlapped_s"], "serialized_s": m["serialized_s"]}
+        t = self.step_transfer_seconds(step)
+        return {"compute_s": compute_s, "transfer_s": t, "overlapped_s": self.end_step(step, compute_s),
+                "serialized_s": step_latency(compute_s, t, overlapped=False)}
+
 
 def generate(config, weights, prompt, steps: int, budget: CacheBudget,
              channel_model: ChannelModel | None = None, mode: str = "sim",
              compute_time_per_step: float = 0.0, prefill_time: float = 0.0,
-             device: int = 0) -> GenerateResult:
-    """engine.py:342-386 on the device."""
+             device: int = 0, clock: str = "logical") -> GenerateResult:
+    """engine.py:342-386 on the device (clock: see the module docstring)."""
     if steps < 1:
         raise ValueError("steps must be >= 1")
     dec = DeviceSpeculativeDecoder(config, weights, budget, channel_model, mode,
-                                   compute_time_per_step, prefill_time, device)
+                                   compute_time_per_step, prefill_time, device, clock)
     try:
         tokens = [dec.prefill(prompt)]
         dec.predecode()
         compute_s = compute_time_per_step
-        pre_t = dec.step_transfer_seconds(0)
-        rows = [{"step": 0, "compute_s": compute_s, "transfer_s": pre_t,
-                 "overlapped_s": dec.end_step(0, compute_s),
-                 "serialized_s": step_latency(compute_s, pre_t, overlapped=False),
+        rows = [{"step": 0, **dec.latency_row(0, compute_s),
                  "bytes": dec.predecode_bytes, "new_pins": dec.predecode_new_pins}]
         logits, metrics = [], []
         for _ in range(steps):
@@ -248,10 +293,7 @@ def generate(config, weights, prompt, steps: int, budget: CacheBudget,
             tokens.append(token)
             logits.append(dec.last_logits[0])
             metrics.append(m)
-            t = dec.step_transfer_seconds(step_idx)
-            rows.append({"step": step_idx, "compute_s": compute_s, "transfer_s": t,
-                         "overlapped_s": dec.end_step(step_idx, compute_s),
-                         "serialized_s": step_latency(compute_s, t, overlapped=False),
+            rows.append({"step": step_idx, **dec.latency_row(step_idx, compute_s),
                          "bytes": m.bytes_fetched, "new_pins": m.new_pins})
         return GenerateResult(tokens=tokens, logits=logits, metrics=metrics, latency_rows=rows,
                               prefill_seconds=prefill_time, total_seconds=prefill_time + dec.clock,

@@ -108,6 +108,23 @@ class DeviceTwoTierCache:
         """'auto' | 'generic' (exact float64 dequant) | 'fast' (tensor cores)."""
         _lib.check(_lib.lib().spc_set_attend_impl(self._h, {"auto": 0, "generic": 1, "fast": 2}[impl]))
 
+    def profile(self, enable: bool) -> dict:
+        """Collect (and reset) the library's CUDA-event timings since the last
+        call, then switch event recording on/off for what follows.  Synchronizes
+        the device.  ms fields: attn = K2 launches, copy = copy-stream work per
+        layer (agg .. host append), wait = exposed prefetch waits on the compute
+        stream, prefetch = PCIe gather kernels; prefetch_bytes = rows moved."""
+        import ctypes as C
+        lib = _lib.lib()
+        am, al, sm, sl, nl = C.c_double(), C.c_int64(), C.c_double(), C.c_int64(), C.c_int64()
+        _lib.check(lib.spc_profile(self._h, int(bool(enable)), C.byref(am), C.byref(al), C.byref(sm),
+                                   C.byref(sl), C.byref(nl)))
+        return {"attn_ms": am.value, "attn_launches": al.value, "copy_ms": sm.value,
+                "copy_launches": sl.value, "launches": nl.value,
+                "wait_ms": float(lib.spc_profile_wait_ms(self._h)),
+                "prefetch_ms": float(lib.spc_profile_prefetch_ms(self._h)),
+                "prefetch_bytes": int(lib.spc_profile_prefetch_bytes(self._h))}
+
     @property
     def device_bytes(self) -> int:
         return int(_lib.lib().spc_device_bytes(self._h))

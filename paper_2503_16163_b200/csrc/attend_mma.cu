@@ -480,6 +480,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
   float vscale[4];  // value K-index (token) scales, q = 2ks + khalf
 #pragma unroll
   for (int q = 0; q < 4; ++q) vscale[q] = cs * pow2i(-(BITS == 2 ? 2 * q : q) - Ev);
+  // PG sz decode: this lane's ks = lane & 1 -> q = 2ks + khalf (kept in registers, no local array)
+  const float vs_lane[2] = {(lane & 1) ? vscale[2] : vscale[0], (lane & 1) ? vscale[3] : vscale[1]};
   // score rows of this lane and their spill rows (aggregate source)
   const int agg_j0 = a.agg_row * G.G;
   int jr[RPL];
@@ -591,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
 #pragma unroll
       for (int slot = 0; slot < 4; ++slot) {
         const float lo = __uint_as_float(vpw[slot] << 16), hi = __uint_as_float(vpw[slot] & 0xFFFF0000u);
-        o[2 * slot] = (hi - lo) * vscale[2 * (lane & 1) + (slot >> 1)];
+        o[2 * slot] = (hi - lo) * vs_lane[slot >> 1];
         o[2 * slot + 1] = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
       }
       ws.sz[2 * lane] = make_float4(o[0], o[1], o[2], o[3]);

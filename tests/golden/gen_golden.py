@@ -17,6 +17,13 @@ cache_<tag>.npz    a TwoTierCache filled with bf16-representable rows: the
 decode_<tag>.npz   the per-layer body of SpeculativeDecoder.decode_step
                    (engine.py:299-321) replayed with reference objects for a
                    few steps, after predecode (engine.py:245-268).
+adapter_<tag>.npz  reference generate() token streams (bf16 hot-path boundary).
+report_toy.spkc    reference `gen-weights --seed 2` weight file (model.py
+                   init_decoder + save_weights).
+report_<tag>.json  reference experiments.run_decode() reports on that file
+                   (bf16 hot-path boundary), plus the arguments used.
+
+    python tests/golden/gen_golden.py [report]   # only the listed groups
 """
 from __future__ import annotations
 
@@ -271,6 +278,51 @@ def gen_adapter(tag, bits, g, r, k, L, prompt_len, steps, seed):
     np.savez_compressed(os.path.join(HERE, f"adapter_{tag}.npz"), **rec)
 
 
+def gen_report():
+    """experiments.run_decode (experiments.py:46-97) on a reference-written
+    weight file, with the same bf16 hot-path boundary as gen_adapter."""
+    import json
+    from speckv import experiments as X
+    from speckv import model as M
+    from speckv import engine as E
+    wpath = os.path.join(HERE, "report_toy.spkc")
+    cfg = M.DecoderConfig(seed=2)
+    M.save_weights(wpath, cfg, M.init_decoder(cfg))
+    orig_qkv, orig_attend = E._qkv, E._attend
+
+    def qkv16(c, lw, x, positions):
+        q, k_, v = orig_qkv(c, lw, x, positions)
+        return bf16_round(q), bf16_round(k_), bf16_round(v)
+
+    def attend16(c, q, keys, vals, mask):
+        out, probs = orig_attend(c, q, keys, vals, mask)
+        return bf16_round(out), probs
+
+    cases = {
+        "b1": dict(prompt=None, prompt_len=12, steps=6, bits=1, group_size=4, k=4, residual=4,
+                   bandwidth=16e9, alpha=5.0, overhead=0.0, compute_s=0.0, mode="sim", seed=0),
+        "b2_seed9": dict(prompt=None, prompt_len=12, steps=8, bits=2, group_size=4, k=6, residual=4,
+                         bandwidth=8e9, alpha=3.0, overhead=1e-6, compute_s=2e-6, mode="sim", seed=9),
+        "b2_prompt": dict(prompt=[1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18], prompt_len=32,
+                          steps=5, bits=2, group_size=4, k=4, residual=4, bandwidth=16e9, alpha=5.0,
+                          overhead=0.0, compute_s=1e-3, mode="thread", seed=0),
+    }
+    E._qkv, E._attend = qkv16, attend16
+    try:
+        for tag, args in cases.items():
+            rep = X.run_decode(weights_path="report_toy.spkc", max_len=4096, **{**args})  # noqa
+            with open(os.path.join(HERE, f"report_{tag}.json"), "w") as fh:
+                json.dump({"args": args, "report": rep}, fh, indent=1)
+    finally:
+        E._qkv, E._attend = orig_qkv, orig_attend
+
+
+if __name__ == "__main__" and len(sys.argv) > 1:
+    os.chdir(HERE)
+    for name in sys.argv[1:]:
+        globals()["gen_" + name]()
+    sys.exit(0)
+
 if __name__ == "__main__":
     gen_quant_groups()
     gen_cache("b2_d128", 2, 2, 128, 32, 32, 8, 200, [0, 5, 37, 100], seed=1)
@@ -286,4 +338,6 @@ if __name__ == "__main__":
     gen_adapter("b2", 2, 4, 4, 4, 4096, 12, 10, seed=3)
     gen_adapter("b1", 1, 4, 4, 4, 4096, 20, 10, seed=4)
     gen_adapter("b16_exact", 16, 4, 8, 1024, 1024, 32, 16, seed=5)
+    os.chdir(HERE)
+    gen_report()
     print("golden fixtures written to", HERE)
