@@ -469,6 +469,117 @@ def run_gpu_arm(args, cfg):
     return 0
 
 
+# model shapes around the hot path for --full-decoder (hidden, ffn, vocab); random-init weights
+MODEL_SHAPES = {"c2": (4096, 11008, 32000),   # LLaMA-2-7B (two-matrix SiLU FFN, engine.py:66-68)
+                "c3": (4096, 14336, 32000),   # Mistral-7B
+                "c1": (4096, 11008, 32000)}
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def run_full_decoder(args, cfg):
+    """the whole model step around the hot path (decoder.py):
+    RMSNorm / QKV GEMM / RoPE / spc_decode_layer / Wo / FFN per layer, logits and
+    argmax for both rows, next tokens fed back on the device.  Random-init bf16
+    weights of the named architecture; the prompt KV is synthetic (prefill_cache).
+    Host slabs are aliased mod host_layers as in the hot-path bench: aliased
+    layers share (and overwrite) one slow-tier slab, which keeps the PCIe
+    traffic and timing identical but makes prefetched row CONTENT approximate."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
+    from paper_2503_16163_b200.decoder import DecoderStack, StackConfig, random_stack
+
+    rank, world, local, local_world = dist_env()
+    torch.cuda.set_device(local)
+    device = f"cuda:{local}"
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(device))
+    hidden, ffn, vocab = MODEL_SHAPES[args.config]
+    sc = StackConfig(layers=cfg["layers"], q_heads=cfg["q_heads"], kv_heads=cfg["kv_heads"],
+                     head_dim=cfg["head_dim"], hidden=hidden, ffn=ffn, vocab=vocab)
+    W, K = args.warmup, args.steps
+    host_layers = args.host_layers or plan_host_layers(cfg, local_world)
+    budget = CacheBudget(bits=cfg["bits"], group_size=cfg["group"], residual=cfg["residual"],
+                         prefetch_k=cfg["topk"], context_length=cfg["ctx"] + W + K + 64)
+    cache = DeviceTwoTierCache(cfg["layers"], cfg["kv_heads"], cfg["head_dim"], budget, batch=cfg["batch"],
+                               q_heads=cfg["q_heads"], device=local, host_layers=host_layers)
+    s0 = torch.randn((host_layers, cfg["batch"], cfg["q_heads"], cfg["head_dim"]), device=device).to(
+        torch.bfloat16)
+    prefill_cache(cache, cfg, host_layers, s0, device, seed=99 + rank)
+    weights = random_stack(sc, device, seed=7 + rank)
+    stack = DecoderStack(sc, weights, cache)
+    B, n = cfg["batch"], cfg["ctx"]
+    gen = torch.Generator(device=device).manual_seed(5 + rank)
+    tok0 = torch.randint(0, vocab, (B,), device=device, generator=gen)
+    pos = torch.full((B,), n, dtype=torch.int32, device=device)
+    spec = stack.predecode(tok0, pos).clone()
+    toks = torch.stack([tok0.to(torch.int32), spec], dim=1)
+    step = 1
+    for _ in range(W):
+        toks = stack.decode_step(step, toks, pos + step - 1).clone()
+        step += 1
+    prof0 = cache.profile(True)
+    del prof0
+    stack.launches = 0
+    torch.cuda.synchronize(device)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record()
+        for _ in range(K):
+            toks = stack.decode_step(step, toks, pos + step - 1).clone()
+            step += 1
+        e1.record()
+        torch.cuda.synchronize(device)
+    elapsed_ms = reduce_max(e0.elapsed_time(e1), device)
+    prof = cache.profile(False)
+    ms_per_step = elapsed_ms / K
+    tokens = whole_job_tokens(B, K, world)
+    value = tokens / (elapsed_ms / 1e3)
+    f = cache.quantized_frontier(0)
+    nn = cache.length(0)
+    kv_bytes = algorithmic_bytes_per_layer(cfg, nn - K // 2, f, cfg["topk"])["hbm"] * cfg["layers"]
+    wbytes = sc.weight_bytes()
+    achieved = (kv_bytes + wbytes) / (ms_per_step / 1e3) / 1e9
+    peak, peak_src = hbm_peak()
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic prompt KV + random-init weights; tokens fed back on device",
+        "config": {"workload": cfg["workload"] + f"; FULL DECODER (hidden {hidden}, ffn {ffn}, vocab {vocab})",
+                   "global_batch": B * world, "seq_len": n, "layers": cfg["layers"],
+                   "parallelism": f"replicas-by-sequence x{world} (no collective)", "host_layers": host_layers,
+                   "l2": "no flush: weights %.1f GB + KV %.1f GB per step >> L2" % (wbytes / 1e9, kv_bytes / 1e9)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_src, "kernel": "whole step (KV + weights)",
+                     "algorithmic_bytes_per_step": kv_bytes + wbytes, "weight_bytes_per_step": wbytes,
+                     "kv_bytes_per_step": kv_bytes},
+        "breakdown_ms_per_step": {"attend_k2": prof["attn_ms"] / K,
+                                  "rest_of_step": ms_per_step - prof["attn_ms"] / K,
+                                  "weights_at_peak": wbytes / peak / 1e6,
+                                  "exposed_prefetch": prof["wait_ms"] / K,
+                                  "prefetch_kernels": prof["prefetch_ms"] / K},
+        "h2d_bytes_per_step": prof["prefetch_bytes"] / K,
+        "gpu_launches": prof["launches"] + stack.launches,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    cache.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -478,12 +589,16 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--host-layers", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--full-decoder", action="store_true",
+                    help="time the whole model step around the hot path (SURVEY 8(f) row 1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = dict(CONFIGS[args.config])
     if args.impl == "reference":
         return run_reference_arm(args, cfg)
+    if args.full_decoder:
+        return run_full_decoder(args, cfg)
     return run_gpu_arm(args, cfg)
 
 

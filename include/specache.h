@@ -81,6 +81,11 @@ SPC_API int spc_cache_destroy(spc_cache* cache);
 SPC_API int spc_cache_fast_path(const spc_cache* cache);
 /* Attention implementation: 0 auto (fast when supported), 1 generic exact, 2 fast (error if unsupported). */
 SPC_API int spc_set_attend_impl(spc_cache* cache, int impl);
+/* K5 (PCIe prefetch gather) sysmem bytes kept in flight, summed over the
+ * batch (0 -> default 256 KiB).  Enough to cover PCIe's bandwidth-delay
+ * product; more only queues in the memory system and slows concurrent kernels
+ * (a full decoder step with GEMMs prefers 128 KiB). */
+SPC_API int spc_set_prefetch_inflight(spc_cache* cache, int64_t bytes);
 SPC_API int64_t spc_device_bytes(const spc_cache* cache);
 SPC_API int64_t spc_host_bytes(const spc_cache* cache);
 
@@ -167,6 +172,29 @@ SPC_API int64_t spc_profile_prefetch_bytes(const spc_cache* cache);
 /* Device pointer + element count of the pin state of (layer): pin_pos int32
  * [batch][units][k] (-1 = empty slot). */
 SPC_API int spc_pin_state(spc_cache* cache, int layer, const int32_t** pin_pos);
+
+/* -- decoder layer around the path ---------------------------
+ * The elementwise pieces of the reference's decoder layer (engine.py:35-72),
+ * fused; the GEMMs are plain cuBLAS bf16 GEMMs on the caller's side.  All
+ * pointers are device pointers; bf16 as uint16 bit patterns. */
+/* x[rows][hidden] fp32 += delta (bf16, may be NULL); out = bf16(x * gain /
+ * sqrt(mean(x^2) + eps)) -- rmsnorm, numerics.py:42-51.  hidden % 8 == 0. */
+SPC_API int spc_add_rmsnorm(float* x, const void* delta, const float* gain, void* out, int rows, int hidden,
+                            float eps, void* stream);
+/* table [rows][d/2] of fp32 (cos, sin) pairs of positions[r] * base^(-2i/d),
+ * angles in fp64 -- rope_apply's angles, numerics.py:54-63.  Positions are
+ * shared by all layers of a step: build once, use in every spc_qkv_rope. */
+SPC_API int spc_rope_table(const int32_t* positions, int rows, int head_dim, double rope_base, float* table,
+                           void* stream);
+/* Split fused QKV GEMM rows [rows][(Hq + 2 Hkv) * d] into q [rows][Hq][d],
+ * k, v [rows][Hkv][d], rotating q and k pairs (2i, 2i+1) by the table --
+ * _qkv + rope_apply, engine.py:39-48, numerics.py:64-70. */
+SPC_API int spc_qkv_rope(const void* qkv, const float* rope_table, int rows, int q_heads, int kv_heads,
+                         int head_dim, void* q, void* k, void* v, void* stream);
+/* g = g / (1 + exp(-g)) in place over n bf16 values (n % 8 == 0) -- _silu, engine.py:35-36. */
+SPC_API int spc_silu(void* g, int64_t n, void* stream);
+/* out[r] = argmax of bf16 row r, ties to the lowest index -- argmax_row, numerics.py:73-78. */
+SPC_API int spc_argmax_rows(const void* x, int rows, int cols, int32_t* out, void* stream);
 
 #ifdef __cplusplus
 }

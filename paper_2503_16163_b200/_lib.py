@@ -59,6 +59,12 @@ _SIGS = {
     "spc_profile_prefetch_bytes": (_I64, [_P]),
     "spc_profile": (_I, [_P, _I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "spc_add_rmsnorm": (_I, [_P, _P, _P, _P, _I, _I, ctypes.c_float, _P]),
+    "spc_set_prefetch_inflight": (_I, [_P, _I64]),
+    "spc_rope_table": (_I, [_P, _I, _I, ctypes.c_double, _P, _P]),
+    "spc_qkv_rope": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "spc_silu": (_I, [_P, _I64, _P]),
+    "spc_argmax_rows": (_I, [_P, _I, _I, _P, _P]),
 }
 
 _lib = None

@@ -108,6 +108,10 @@ class DeviceTwoTierCache:
         """'auto' | 'generic' (exact float64 dequant) | 'fast' (tensor cores)."""
         _lib.check(_lib.lib().spc_set_attend_impl(self._h, {"auto": 0, "generic": 1, "fast": 2}[impl]))
 
+    def set_prefetch_inflight(self, nbytes: int) -> None:
+        """K5 sysmem bytes in flight over the batch (0 = default 256 KiB)."""
+        _lib.check(_lib.lib().spc_set_prefetch_inflight(self._h, int(nbytes)))
+
     def profile(self, enable: bool) -> dict:
         """Collect (and reset) the library's CUDA-event timings since the last
         call, then switch event recording on/off for what follows.  Synchronizes

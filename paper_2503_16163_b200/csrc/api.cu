@@ -34,6 +34,16 @@ int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
+}  // namespace
+
+namespace spc {
+int set_error(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+}  // namespace spc
+
+namespace {
 #define CUDA_TRY(expr)                                                               \
   do {                                                                               \
     cudaError_t _e = (expr);                                                         \
@@ -51,6 +61,7 @@ struct spc_cache {
   Geo G{};
   int device = 0;
   int impl = 0;  // 0 auto, 1 generic exact, 2 fast
+  int64_t pf_inflight = int64_t(256) << 10;  // K5 sysmem bytes in flight (spc_set_prefetch_inflight)
   std::vector<LayerBufs> L;
   std::vector<void*> dev_allocs;
   __nv_bfloat16* host_k = nullptr;
@@ -222,7 +233,8 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
     q1 = prof_event(c);
     CUDA_TRY(cudaEventRecord(q0, cs));
   }
-  launch_prefetch(G, c->L[layer], host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer), cs);
+  launch_prefetch(G, c->L[layer], host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer), c->pf_inflight,
+                  cs);
   if (c->prof) {
     CUDA_TRY(cudaEventRecord(q1, cs));
     c->prof_pf.push_back({q0, q1});
@@ -427,6 +439,13 @@ int64_t spc_row_bytes(const spc_cache* c, int64_t positions) {
 int spc_set_attend_impl(spc_cache* c, int impl) {
   if (!c || impl < 0 || impl > 2) return fail(SPC_EINVAL, "impl must be 0 (auto), 1 (generic) or 2 (fast)");
   c->impl = impl;
+  return SPC_OK;
+}
+
+int spc_set_prefetch_inflight(spc_cache* c, int64_t bytes) {
+  if (!c) return fail(SPC_EINVAL, "null cache");
+  if (bytes < 0) return fail(SPC_EINVAL, "prefetch in-flight bytes must be >= 0");
+  c->pf_inflight = bytes ? bytes : int64_t(256) << 10;
   return SPC_OK;
 }
 

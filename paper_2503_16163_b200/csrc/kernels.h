@@ -57,7 +57,7 @@ void launch_select(const float* scores, int n, int k, int32_t* out, cudaStream_t
 void launch_set_pins(const Geo& G, const LayerBufs& B, int seq, int unit, const int32_t* pos,
                      int npos, cudaStream_t st);
 void launch_prefetch(const Geo& G, const LayerBufs& B, const __nv_bfloat16* host_k,
-                     const __nv_bfloat16* host_v, cudaStream_t st);
+                     const __nv_bfloat16* host_v, int64_t inflight_bytes, cudaStream_t st);
 void launch_prefetch_one(const Geo& G, const LayerBufs& B, int seq, int unit,
                          const __nv_bfloat16* host_k, const __nv_bfloat16* host_v, cudaStream_t st);
 void launch_copy_pins(const Geo& G, const LayerBufs& B, int seq, int unit, const __nv_bfloat16* k_rows,
@@ -68,5 +68,8 @@ void launch_host_append(const Geo& G, const LayerBufs& B, int n, __nv_bfloat16* 
                         __nv_bfloat16* host_v, cudaStream_t st);
 void launch_ring_fill(const Geo& G, const LayerBufs& B, const __nv_bfloat16* K,
                       const __nv_bfloat16* V, int n, int f, cudaStream_t st);
+
+// spc_last_error() text for entry points outside api.cu (layer.cu)
+int set_error(int code, const char* msg);
 
 }  // namespace spc

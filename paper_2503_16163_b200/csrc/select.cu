@@ -13,6 +13,7 @@
 //
 // K6 replaces append_verified (kvcache.py:162-171): row 0's K/V go to the
 // residual ring (HBM) and to the slow tier (pinned host, zero-copy store).
+#include <cstdlib>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -244,14 +245,12 @@ void launch_set_pins(const Geo& G, const LayerBufs& B, int seq, int unit, const 
 }
 
 // K5: PCIe gather of the new pins (zero-copy loads from the pinned host tier).
-// A small grid (kPfCtas CTA per (seq, unit)): a resident prefetch CTA costs its SM
-// one K2 CTA slot (registers) for the whole PCIe-bound gather, so keep few, while
-// each thread keeps kPfUnroll independent 16-byte host loads in flight, enough
-// to cover PCIe latency at full link rate.  Rows of a unit's heads are
-// contiguous in the host tier ([pos][H][d]).
-constexpr int kPfCtas = 1;
-constexpr int kPfUnroll = 16;
+// Few CTAs (a resident prefetch CTA costs its SM a K2 slot for the whole
+// PCIe-bound gather), each thread keeping kPfUnroll independent 16-byte host
+// loads of K and V in flight.  Rows of a unit's heads are contiguous in the host
+// tier ([pos][H][d]).
 
+template <int kPfUnroll>
 __global__ void __launch_bounds__(256) k_prefetch(Geo G, LayerBufs B, const uint4* host_k,
                                                   const uint4* host_v, int seq0, int unit0, int one) {
   const int bu_i = one ? 0 : blockIdx.y;
@@ -303,16 +302,33 @@ __global__ void __launch_bounds__(256) k_prefetch(Geo G, LayerBufs B, const uint
   }
 }
 
+// Sysmem reads in flight = grid CTAs * 256 threads * depth * 32 B (K + V).  PCIe
+// only needs its bandwidth-delay product (~150-250 KB); anything beyond queues in
+// the memory system and slows every concurrent HBM client (measured: K2 -4%,
+// cuBLAS GEMMs / small kernels up to 10x with 2 MB in flight).  So the grid and
+// depth are sized from a byte budget, independent of batch size.
+static void launch_pf(int64_t inflight, int units, const Geo& G, const LayerBufs& B, const __nv_bfloat16* host_k,
+                      const __nv_bfloat16* host_v, int seq, int unit, int one, cudaStream_t st) {
+  const uint4* hk = reinterpret_cast<const uint4*>(host_k);
+  const uint4* hv = reinterpret_cast<const uint4*>(host_v);
+  const int64_t per = inflight / units;            // bytes per (seq, unit)
+  const int64_t cta2 = 256 * 32 * 2;               // one CTA at depth 2
+  if (per >= cta2) {
+    const int ctas = (int)(per / cta2 < 16 ? per / cta2 : 16);
+    k_prefetch<2><<<dim3(ctas, one ? 1 : units), 256, 0, st>>>(G, B, hk, hv, seq, unit, one);
+  } else {
+    k_prefetch<1><<<dim3(1, one ? 1 : units), 256, 0, st>>>(G, B, hk, hv, seq, unit, one);
+  }
+}
+
 void launch_prefetch(const Geo& G, const LayerBufs& B, const __nv_bfloat16* host_k,
-                     const __nv_bfloat16* host_v, cudaStream_t st) {
-  k_prefetch<<<dim3(kPfCtas, G.U * G.batch), 256, 0, st>>>(
-      G, B, reinterpret_cast<const uint4*>(host_k), reinterpret_cast<const uint4*>(host_v), 0, 0, 0);
+                     const __nv_bfloat16* host_v, int64_t inflight, cudaStream_t st) {
+  launch_pf(inflight, G.U * G.batch, G, B, host_k, host_v, 0, 0, 0, st);
 }
 
 void launch_prefetch_one(const Geo& G, const LayerBufs& B, int seq, int unit,
                          const __nv_bfloat16* host_k, const __nv_bfloat16* host_v, cudaStream_t st) {
-  k_prefetch<<<dim3(kPfCtas, 1), 256, 0, st>>>(
-      G, B, reinterpret_cast<const uint4*>(host_k), reinterpret_cast<const uint4*>(host_v), seq, unit, 1);
+  launch_pf(int64_t(256) << 10, 1, G, B, host_k, host_v, seq, unit, 1, st);
 }
 
 // pin() with caller-supplied rows: device bf16 [npos][Hu][d] -> slots 0..npos-1
