@@ -48,7 +48,14 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int kStages = 3;
+#ifndef SPC_K2_STAGES
+#define SPC_K2_STAGES 3
+#endif
+#ifndef SPC_K2_MINB
+#define SPC_K2_MINB 2
+#endif
+constexpr int kStages = SPC_K2_STAGES;  // TMA ring depth per warp
+constexpr int kMinBlocks = SPC_K2_MINB; // resident CTAs per SM
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -150,9 +157,19 @@ struct StageLayout {
 
 template <int BITS, int NR>
 struct __align__(16) WarpSmem {
-  uint4 bk[8][4 * NR];  // key B fragments {b0hi, b1hi, b0lo, b1lo} of lane (row j, t'), [ks][4j + (t' ^ (ks&3))]
+  // key B fragments {b0hi, b1hi, b0lo, b1lo} of lane (row j, t'), [ks][4j + (t' ^ ((ks>>1)&3))];
+  // row stride = 4 mod 8 uint4 so a 128-bit store phase (ks = 0..7) hits 8 distinct bank slots
+  static constexpr int kBkRow = 4 * NR + ((NR & 1) ? 0 : 4);
+  uint4 bk[8][kBkRow];
   uint32_t stage[kStages][StageLayout<BITS>::words];      // TMA ring
-  float P[NR][33];                                        // block probabilities [row][token]
+  // block probabilities: PG (<= 2 rows) [row][33]; otherwise [row & 1][token][row >> 1]
+  // in 132-float planes, conflict-free for both the score-side stores (t = c+gq,
+  // row = 2tq+e) and the value-side loads (row = gq, t = c+2tq)
+  static constexpr int kPWords = NR * 4 <= 8 ? NR * 33 : 2 * 132;
+  float P[kPWords];
+  __device__ static constexpr int pidx(int row, int t) {
+    return NR * 4 <= 8 ? row * 33 + t : (row & 1) * 132 + t * 4 + (row >> 1);
+  }
   float4 sz[64];                                          // value (s*2^-q, z) pairs, vparams order
   uint64_t bar[kStages];
 };
@@ -396,7 +413,7 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
 }
 
 template <int BITS, int NR>
-__global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a) {
   // PACK: score MMA columns n = 2*row + plane (hi/lo of each row side by side),
   //       one MMA per k-step and one score row per lane (row = lane & 3).
   // PG:   P.V columns n = group*NR + row, one B fragment for all value groups.
@@ -561,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
           split2(w0, w2, frag.x, frag.z);
           split2(w1, w3, frag.y, frag.w);
         }
-        ws.bk[kks][4 * j + (ktk ^ (kks & 3))] = frag;
+        ws.bk[kks][4 * j + (ktk ^ ((kks >> 1) & 3))] = frag;
       }
       // reduce-scatter of the NR per-lane partials: after log2(NR) halving steps a
       // lane holds one row, r = lane >> (5 - log2 NR); the remaining butterflies
@@ -628,11 +645,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
       uint32_t b0, b1, b2 = 0, b3 = 0;
       if (PACK) {  // column n = gq = 2*row + plane; rows >= NR are zero columns
         uint2 bb = make_uint2(0, 0);
-        if ((gq >> 1) < NR) bb = reinterpret_cast<const uint2*>(&ws.bk[ks][4 * (gq >> 1) + (tq ^ (ks & 3))])[gq & 1];
+        if ((gq >> 1) < NR) bb = reinterpret_cast<const uint2*>(&ws.bk[ks][4 * (gq >> 1) + (tq ^ ((ks >> 1) & 3))])[gq & 1];
         b0 = bb.x;
         b1 = bb.y;
       } else {
-        const uint4 bb = ws.bk[ks][4 * gq + (tq ^ (ks & 3))];
+        const uint4 bb = ws.bk[ks][4 * gq + (tq ^ ((ks >> 1) & 3))];
         b0 = bb.x;
         b1 = bb.y;
         b2 = bb.z;
@@ -759,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         for (int e = 0; e < RPL; ++e) {
           const float p = fast_exp2(sc[mt][hf][e] - m_run[e]);
           l_run[e] += p;
-          if (jr[e] < NR) ws.P[jr[e]][T] = p;
+          if (jr[e] < NR) ws.P[WarpSmem<BITS, NR>::pidx(jr[e], T)] = p;
         }
       }
     }
@@ -815,7 +832,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
         for (int slot = 0; slot < 4; ++slot) {
           const int khalf = slot >> 1;
           const int t = 16 * ks + 2 * tq + (slot & 1) + 8 * khalf;
-          const float p = live ? ws.P[prow][t] : 0.f;
+          const float p = live ? ws.P[WarpSmem<BITS, NR>::pidx(prow, t)] : 0.f;
           zacc[gi] = fmaf(p, zz4[slot], zacc[gi]);
           x[slot] = p * spr4[slot];
         }
@@ -872,7 +889,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend_fast(AttnArgs a) {
           const int t = 16 * ks + 2 * tq + (slot & 1) + 8 * khalf;
           const uint32_t w = vpw[4 * ks + slot];
           const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xFFFF0000u);
-          const float p = live ? ws.P[prow][t] : 0.f;
+          const float p = live ? ws.P[WarpSmem<BITS, NR>::pidx(prow, t)] : 0.f;
           const float z = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
           zacc[gi] = fmaf(p, z, zacc[gi]);
           x[slot] = p * (hi - lo) * vscale[2 * ks + khalf];
@@ -1036,7 +1053,7 @@ template <int BITS, int NR>
 void launch_fast_t(const AttnArgs& a, cudaStream_t st) {
   constexpr size_t smem = fast_smem_bytes<BITS, NR>();
   // two CTAs per SM (228 KB, 1 KB reserved per CTA) is the design point
-  static_assert((BITS == 2 && NR == 8) || smem <= 113 * 1024, "K2 shared memory exceeds 2 CTAs/SM");
+  static_assert((BITS == 2 && NR == 8) || smem * kMinBlocks <= 227 * 1024, "K2 shared memory exceeds kMinBlocks CTAs/SM");
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_attend_fast<BITS, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
