@@ -196,6 +196,28 @@ SPC_API int spc_silu(void* g, int64_t n, void* stream);
 /* out[r] = argmax of bf16 row r, ties to the lowest index -- argmax_row, numerics.py:73-78. */
 SPC_API int spc_argmax_rows(const void* x, int rows, int cols, int32_t* out, void* stream);
 
+/* -- hit-rate study on the device -----------------------------
+ * A trace row (sequence s, query step t) starts at rows + s*seq_ld + t*row_ld
+ * and holds lens[t] fp32 probabilities; a sequence is one (layer, q head) of
+ * AttentionTrace.sequences() (hitrate.py:23-25).  lens is a DEVICE int32
+ * array of `steps` entries, max_len its maximum.  Rates are float64 and
+ * bit-identical to hitrate.py on the same rows (see csrc/hitrate.cu). */
+/* Exact fp32 attention of one decode step over a full cache (the full-cache
+ * decoder's _attend, engine.py:51-63): q [q_heads][d], k/v [n][kv_heads][d]
+ * fp32; writes out [q_heads][d] and the probability row of q head h to
+ * probs + h*probs_ld (the trace row of that step). */
+SPC_API int spc_full_attend(const float* q, const float* k, const float* v, int n, int q_heads, int kv_heads,
+                            int head_dim, float scale, float* out, float* probs, int64_t probs_ld, void* stream);
+/* sums[s*steps + t] = float32 np.sum of the row -- AttentionTrace.validate, hitrate.py:27-31. */
+SPC_API int spc_trace_row_sums(const float* rows, int64_t seq_ld, int64_t row_ld, const int32_t* lens, int nseq,
+                               int steps, int max_len, double* sums, void* stream);
+/* rates[s*steps + t] = mass of the k largest entries -- topk_hitrate, hitrate.py:34-43. */
+SPC_API int spc_topk_hitrate(const float* rows, int64_t seq_ld, int64_t row_ld, const int32_t* lens, int nseq,
+                             int steps, int max_len, int k, double* rates, void* stream);
+/* rates[s*steps + t] = greedy cumulative-score eviction at budget k -- eviction_hitrate, hitrate.py:46-77. */
+SPC_API int spc_eviction_hitrate(const float* rows, int64_t seq_ld, int64_t row_ld, const int32_t* lens, int nseq,
+                                 int steps, int max_len, int k, double* rates, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

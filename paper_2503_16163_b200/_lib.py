@@ -65,6 +65,10 @@ _SIGS = {
     "spc_qkv_rope": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
     "spc_silu": (_I, [_P, _I64, _P]),
     "spc_argmax_rows": (_I, [_P, _I, _I, _P, _P]),
+    "spc_full_attend": (_I, [_P, _P, _P, _I, _I, _I, _I, ctypes.c_float, _P, _P, _I64, _P]),
+    "spc_trace_row_sums": (_I, [_P, _I64, _I64, _P, _I, _I, _I, _P, _P]),
+    "spc_topk_hitrate": (_I, [_P, _I64, _I64, _P, _I, _I, _I, _I, _P, _P]),
+    "spc_eviction_hitrate": (_I, [_P, _I64, _I64, _P, _I, _I, _I, _I, _P, _P]),
 }
 
 _lib = None

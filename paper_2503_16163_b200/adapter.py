@@ -29,6 +29,7 @@ import numpy as np
 from .budget import CacheBudget
 from .cache import DeviceTwoTierCache
 from .decode import SpeculativeLayerDecoder, StepMetrics
+from .toymodel import ToyModel
 from .transfer import ChannelModel, ProtocolError, step_latency, transfer_time
 
 __all__ = ["DeviceSpeculativeDecoder", "GenerateResult", "generate"]
@@ -46,7 +47,7 @@ class GenerateResult:
     decoder: "DeviceSpeculativeDecoder" = None
 
 
-class DeviceSpeculativeDecoder:
+class DeviceSpeculativeDecoder(ToyModel):
     """engine.py:186-339 on the device cache.  `config` / `weights` are the
     reference's DecoderConfig / Weights (or any objects with the same fields)."""
 
@@ -61,14 +62,8 @@ class DeviceSpeculativeDecoder:
         self.clock_mode = clock
         self._measured: dict[int, dict] = {}
         self._ev = None
-        torch.backends.cuda.matmul.allow_tf32 = False  # fp32 model math, as the reference
-        self.config, self.budget = config, budget
-        self.dev = f"cuda:{device}"
-        T = lambda a: torch.as_tensor(np.asarray(a, np.float32), device=self.dev)
-        self.emb = T(weights.embedding)
-        self.lw = [{k: T(getattr(lw, k)) for k in ("wq", "wk", "wv", "wo", "attn_norm", "ffn_norm", "w1", "w2")}
-                   for lw in weights.layers]
-        self.final_norm, self.head = T(weights.final_norm), T(weights.head)
+        ToyModel.__init__(self, config, weights, device)
+        self.budget = budget
         self.cache = DeviceTwoTierCache(config.layers, config.kv_heads, config.head_dim, budget,
                                         q_heads=config.q_heads, device=device)
         self.layer_dec = SpeculativeLayerDecoder(self.cache)
@@ -85,51 +80,16 @@ class DeviceSpeculativeDecoder:
         self.predecode_bytes = 0
         self.predecode_new_pins = 0
         self.last_logits = None
-        d = config.head_dim
-        idx = np.arange(d // 2, dtype=np.float64)
-        self._inv_freq = config.rope_base ** (-2.0 * idx / d)
 
     def close(self) -> None:
         self.cache.close()
 
-    # -- toy model pieces (fp32, on device) ---------------------------------------------
-    def _rmsnorm(self, x, gain, eps=1e-6):
-        import torch
-        ms = torch.mean(x * x, dim=-1, keepdim=True)
-        return x * gain / torch.sqrt(ms + eps)
-
-    def _rope(self, x, positions):
-        import torch
-        ang = np.outer(np.asarray(positions, np.float64), self._inv_freq)  # float64 like numerics.py:62
-        cos = torch.as_tensor(np.cos(ang).astype(np.float32), device=self.dev)[:, None, :]
-        sin = torch.as_tensor(np.sin(ang).astype(np.float32), device=self.dev)[:, None, :]
-        x0, x1 = x[..., 0::2], x[..., 1::2]
-        out = torch.empty_like(x)
-        out[..., 0::2] = x0 * cos - x1 * sin
-        out[..., 1::2] = x0 * sin + x1 * cos
-        return out
-
     def _qkv(self, lw, x, positions):
         """engine.py:39-48, then rounded to bf16 at the hot-path boundary."""
         import torch
-        cfg = self.config
-        n = x.shape[0]
-        xn = self._rmsnorm(x, lw["attn_norm"])
-        q = (xn @ lw["wq"]).reshape(n, cfg.q_heads, cfg.head_dim)
-        k = (xn @ lw["wk"]).reshape(n, cfg.kv_heads, cfg.head_dim)
-        v = (xn @ lw["wv"]).reshape(n, cfg.kv_heads, cfg.head_dim)
-        q, k = self._rope(q, positions), self._rope(k, positions)
+        q, k, v = self._qkv_f32(lw, x, positions)
         bf = lambda t: t.to(torch.bfloat16)
         return bf(q), bf(k), bf(v)
-
-    def _ffn(self, lw, x):
-        import torch
-        xn = self._rmsnorm(x, lw["ffn_norm"])
-        g = xn @ lw["w1"]
-        return x + (g / (1.0 + torch.exp(-g))) @ lw["w2"]
-
-    def _logits(self, x):
-        return self._rmsnorm(x, self.final_norm) @ self.head
 
     # -- phases (engine.py:220-339) --------------------------------------------------------
     def prefill(self, prompt) -> int:

@@ -1,4 +1,4 @@
-"""`python -m paper_2503_16163_b200 {gen-weights,decode}`.
+"""`python -m paper_2503_16163_b200 {gen-weights,decode,hitrate}`.
 
 The reference's `speckv gen-weights` / `speckv decode` UX (src/speckv/cli.py:
 71-120: same options, defaults, JSON/CSV/--out emission) running in-process on
@@ -98,6 +98,30 @@ def decode(weights_path, prompt, prompt_len, steps, bits, group_size, k, residua
                             bandwidth, alpha, overhead, compute_s, mode, seed, max_len=max_len,
                             clock=clock, device=device)
     except (ValueError, OSError, ProtocolError) as exc:
+        raise click.ClickException(str(exc))
+    _emit(report, as_csv, out)
+
+
+@main.command()
+@click.argument("weights_path")
+@click.option("--prompt", default=None, help="Comma-separated token ids.")
+@click.option("--prompt-len", default=32, type=int)
+@click.option("--steps", default=32, type=int)
+@click.option("--k-sweep", default="1,4,16,64", help="Comma-separated k values.")
+@click.option("--seed", default=0, type=int)
+@click.option("--max-len", default=4096, type=int)
+@click.option("--device", default=0, type=int)
+@click.option("--json", "as_json", flag_value=True, default=True, help="Full report as JSON (default).")
+@click.option("--csv", "as_csv", is_flag=True, default=False, help="Report rows as CSV.")
+@click.option("--out", default=None, help="Write output to a file.")
+def hitrate(weights_path, prompt, prompt_len, steps, k_sweep, seed, max_len, device, as_json, as_csv, out):
+    """Top-k vs greedy-eviction hit-rate curves from a traced decode (cli.py:128-146)."""
+    from .hitrate import hitrate_experiment
+    ids = [int(t) for t in prompt.split(",")] if prompt else None
+    try:
+        report = hitrate_experiment(weights_path, ids, prompt_len, steps, [int(v) for v in k_sweep.split(",")],
+                                    seed, max_len=max_len, device=device)
+    except (ValueError, OSError) as exc:
         raise click.ClickException(str(exc))
     _emit(report, as_csv, out)
 

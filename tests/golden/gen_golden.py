@@ -22,6 +22,11 @@ report_toy.spkc    reference `gen-weights --seed 2` weight file (model.py
                    init_decoder + save_weights).
 report_<tag>.json  reference experiments.run_decode() reports on that file
                    (bf16 hot-path boundary), plus the arguments used.
+hitrate_rows.npz   random attention-trace sequences (flat, peaky, tied and
+                   growing rows) with the reference topk_hitrate /
+                   eviction_hitrate over a k sweep (hitrate.py:34-77).
+hitrate_report.json reference experiments.hitrate_experiment() on
+                   report_toy.spkc (FullCacheDecoder trace, experiments.py:100-137).
 
     python tests/golden/gen_golden.py [report]   # only the listed groups
 """
@@ -317,6 +322,46 @@ def gen_report():
         E._qkv, E._attend = orig_qkv, orig_attend
 
 
+def gen_hitrate():
+    """hitrate.py on synthetic traces + experiments.hitrate_experiment."""
+    import json
+    from speckv import experiments as X
+    from speckv import hitrate as Hr
+    rng = np.random.default_rng(11)
+    seqs = []
+    for kind in ("flat", "peaky", "tied", "sparse", "short"):
+        n0 = {"short": 1, "sparse": 40}.get(kind, 150)
+        steps = 9
+        rows = []
+        for t in range(steps):
+            n = n0 + t
+            if kind == "flat":
+                x = rng.random(n).astype(np.float32)
+            elif kind == "peaky":
+                x = np.exp(3.0 * rng.standard_normal(n)).astype(np.float32)
+            elif kind == "tied":
+                x = rng.integers(1, 4, n).astype(np.float32)
+            elif kind == "sparse":
+                x = np.where(rng.random(n) < 0.3, rng.random(n), 0.0).astype(np.float32)
+                x[0] = 1.0
+            else:
+                x = rng.random(n).astype(np.float32)
+            rows.append((x / x.sum(dtype=np.float32)).astype(np.float32))
+        seqs.append(rows)
+    ks = [0, 1, 2, 3, 5, 16, 64, 1000]
+    rec = {"ks": np.asarray(ks, np.int64), "nseq": np.int64(len(seqs))}
+    for i, rows in enumerate(seqs):
+        rec[f"lens_{i}"] = np.asarray([r.size for r in rows], np.int64)
+        rec[f"rows_{i}"] = np.concatenate(rows)
+        rec[f"topk_{i}"] = np.stack([Hr.topk_hitrate(rows, k) for k in ks])
+        rec[f"evict_{i}"] = np.stack([Hr.eviction_hitrate(rows, k) for k in ks])
+    np.savez_compressed(os.path.join(HERE, "hitrate_rows.npz"), **rec)
+    args = dict(prompt=None, prompt_len=12, steps=6, k_sweep=[1, 4, 16, 64], seed=0)
+    rep = X.hitrate_experiment(weights_path="report_toy.spkc", max_len=4096, **args)
+    with open(os.path.join(HERE, "hitrate_report.json"), "w") as fh:
+        json.dump({"args": args, "report": rep}, fh, indent=1)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
     os.chdir(HERE)
     for name in sys.argv[1:]:
@@ -340,4 +385,5 @@ if __name__ == "__main__":
     gen_adapter("b16_exact", 16, 4, 8, 1024, 1024, 32, 16, seed=5)
     os.chdir(HERE)
     gen_report()
+    gen_hitrate()
     print("golden fixtures written to", HERE)
