@@ -44,6 +44,12 @@ CONFIGS = {
                         "1-bit KV (g32, r64), top-k 128",
                layers=32, batch=8, kv_heads=8, q_heads=32, head_dim=128, ctx=131072, bits=1,
                group=32, residual=64, topk=128),
+    # BASELINE.json configs[3], one rank's share: global batch 32 over 8 GPUs -> 4
+    # sequences per rank (sequence sharding); `--gpus 8` under torchrun is C4 itself
+    "c4": dict(workload="C4: LLaMA-3-8B-shaped GQA (8 KV heads) 32-layer decode, ctx 128k, global batch 32 "
+                        "over 8 GPUs (4 per rank), 1-bit KV (g32, r64), top-k 256, full bf16 cache in pinned host",
+               layers=32, batch=4, kv_heads=8, q_heads=32, head_dim=128, ctx=131072, bits=1,
+               group=32, residual=64, topk=256),
     # BASELINE.json configs[0] (parity config; launch-bound)
     "c1": dict(workload="C1: single-layer SpeCache decode, 32 heads x d128, ctx 4096, 2-bit KV, "
                         "top-k 64, residual 32, batch 1",

@@ -56,6 +56,17 @@ constexpr int kThreads = kWarps * 32;
 #endif
 constexpr int kStages = SPC_K2_STAGES;  // TMA ring depth per warp
 constexpr int kMinBlocks = SPC_K2_MINB; // resident CTAs per SM
+#ifndef SPC_K2_LAZY
+#define SPC_K2_LAZY 1
+#endif
+// Lazy online-softmax rescale (SPC_K2_LAZY): the running max m_run is only
+// raised (warp reduction + accumulator rescale) when some score exceeds it by
+// more than kSlack (log2 units); otherwise P = exp2(s - m_run) <= 2^kSlack is
+// used as is.  (O, l) are scaled consistently, so the result is the same
+// softmax; the per-block max reduction (3 dependent SHFL+FMNMX levels per
+// row) disappears from the common path.
+constexpr int kSlackLog2 = SPC_K2_LAZY ? 8 : 0;  // P <= 2^kSlackLog2
+constexpr float kSlack = (float)kSlackLog2;
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -489,7 +500,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   const float rk = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 2 + 0]) * cs;
   const float rv = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 2 + 1]) * cs;
   const int Ek = (qabs * rk > 0.f) ? ceil_log2(qabs * rk) - 14 : 0;
-  const int Ev = (rv > 0.f) ? ceil_log2(rv) - 14 : 0;
+  // lazy softmax rescale: P = exp2(s - m_run) may reach 2^kSlack, so the value
+  // B exponent keeps kSlack bits of headroom (max|P*s'| <= 2^14 still)
+  const int Ev = (rv > 0.f) ? ceil_log2(rv) - 14 + kSlackLog2 : 0;
   const int sp = BITS == 2 ? 2 * (kks & 3) : kks;       // K-index (channel) scale of this lane
   const float kscale = cs * pow2i(-sp - Ek);              // (hi-lo) -> s * 2^(-sp-Ek)
   const float k_out = pow2i(24 + Ek);                     // D * k_out = sum_c code * Q * s
@@ -729,22 +742,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
           }
       }
     }
-    float mn[RPL];
+    float mloc[RPL];
     bool grow = false;
 #pragma unroll
     for (int e = 0; e < RPL; ++e) {
-      float mx = fmaxf(fmaxf(sc[0][0][e], sc[0][1][e]), fmaxf(sc[1][0][e], sc[1][1][e]));
-      mx = warp_max_g(mx);
-      mn[e] = fmaxf(m_run[e], mx);
-      grow |= mn[e] > m_run[e];
+      mloc[e] = fmaxf(fmaxf(sc[0][0][e], sc[0][1][e]), fmaxf(sc[1][0][e], sc[1][1][e]));
+      grow |= mloc[e] > m_run[e] + kSlack;  // -inf + kSlack = -inf: any finite score grows
     }
     if (__any_sync(0xffffffffu, grow)) {
       float al[RPL];
 #pragma unroll
       for (int e = 0; e < RPL; ++e) {
-        al[e] = m_run[e] == -CUDART_INF_F ? 0.f : fast_exp2(m_run[e] - mn[e]);
+        const float mn = fmaxf(m_run[e], warp_max_g(mloc[e]));
+        al[e] = m_run[e] == -CUDART_INF_F ? 0.f : fast_exp2(m_run[e] - mn);
         l_run[e] *= al[e];
-        m_run[e] = mn[e];
+        m_run[e] = mn;
       }
       // value accumulator columns n = 2tq + e' and the z role of this lane
       float ac[2], az;
@@ -774,7 +786,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
         const int T = 16 * mt + gq + 8 * hf;
 #pragma unroll
         for (int e = 0; e < RPL; ++e) {
-          const float p = fast_exp2(sc[mt][hf][e] - m_run[e]);
+          // m_run = -inf only while every score so far is masked: P = 0, not exp2(NaN)
+          const float p = fast_exp2(sc[mt][hf][e] - (m_run[e] == -CUDART_INF_F ? 0.f : m_run[e]));
           l_run[e] += p;
           if (jr[e] < NR) ws.P[WarpSmem<BITS, NR>::pidx(jr[e], T)] = p;
         }
