@@ -195,7 +195,7 @@ struct MergeSmem {
 // exact segment scratch (split == nsplit CTAs)
 template <int NR>
 struct ExactSmem {
-  static constexpr int CH = 256;
+  static constexpr int CH = 512;
   float sc[NR][CH];
   float fac[NR], m[NR], l[NR], pm[NR], pl[NR];
   int slots[1024];
@@ -211,9 +211,13 @@ constexpr size_t fast_smem_bytes() {
 }
 
 // ---- exact segment: pinned slots + residual ring + in-step rows (bf16, exact) ----------
-// 8 warps; a warp scores one row at a time (lane = 4 channels), rows in chunks of
-// 256 with an online softmax; pinned rows first so their (m, l) gives the pinned
-// mass (engine.py:314-316).
+// One CTA per (seq, kv head), 8 warps, latency-oriented: a warp scores kRows
+// rows per batch with every row's 8-byte key load issued before any math, and
+// the NR x kRows per-lane partial dot products are finished by one warp
+// reduce-scatter (V-1 shuffles for V values instead of 5 per value).  Rows are
+// processed in chunks of CH with an online softmax; the pinned rows' own
+// (max, sum) -- the pinned mass, engine.py:314-316 -- is tracked alongside, so
+// pinned and residual rows share one chunk.
 template <int NR>
 __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int h, const int b,
                                    unsigned char* smem) {
@@ -221,6 +225,10 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
   const LayerBufs& B = a.B;
   ExactSmem<NR>& ex = *reinterpret_cast<ExactSmem<NR>*>(smem);
   constexpr int CH = ExactSmem<NR>::CH;
+  constexpr int kRows = NR <= 2 ? 4 : 16 / NR;  // rows per warp batch (measured best; NR=8 spill-free)
+  constexpr int V = NR * kRows;                  // partial sums per lane per batch: 4, 8 or 16
+  constexpr int LV = V == 4 ? 2 : V == 8 ? 3 : 4;
+  static_assert(V == (1 << LV), "reduce-scatter needs a power-of-two value count");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int unit = G.scope ? h : 0, hh = G.scope ? 0 : h;
   float Qr[NR][4];
@@ -259,6 +267,7 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
 #pragma unroll
   for (int j = 0; j < NR; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
 
+  // row `it` (0 <= it < total): pinned slots, then residual positions, then the in-step rows
   auto row_ptr = [&](int it, const __nv_bfloat16*& kr, const __nv_bfloat16*& vr, int& pos, bool& spec) {
     spec = false;
     pos = -1;
@@ -282,72 +291,103 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
     }
   };
 
-  for (int c0 = 0; c0 < total;) {
-    int cend = min(total, c0 + CH);
-    if (c0 < npin) cend = min(cend, npin);
-    const int count = cend - c0;
-    // scores: each warp keeps kRows rows in flight (independent 8-byte loads per
-    // lane), then reduces them over the warp
-    constexpr int kRows = 4;
+  for (int c0 = 0; c0 < total; c0 += CH) {
+    const int count = min(total, c0 + CH) - c0;
+    // ---- scores: kRows rows per warp batch, loads first, one reduce-scatter
     for (int it0 = warp; it0 < count; it0 += kWarps * kRows) {
-      float k4[kRows][4];
+      uint2 kw[kRows];
       int posr[kRows];
       bool specr[kRows];
 #pragma unroll
       for (int u = 0; u < kRows; ++u) {
         const int it = it0 + u * kWarps;
-        k4[u][0] = k4[u][1] = k4[u][2] = k4[u][3] = 0.f;
+        kw[u] = make_uint2(0u, 0u);
         posr[u] = -1;
         specr[u] = false;
         if (it < count) {
           const __nv_bfloat16 *kr, *vr;
           row_ptr(c0 + it, kr, vr, posr[u], specr[u]);
-          const uint2 w = *reinterpret_cast<const uint2*>(kr + 4 * lane);
-          const __nv_bfloat162 k01 = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
-          const __nv_bfloat162 k23 = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
-          k4[u][0] = __low2float(k01);
-          k4[u][1] = __high2float(k01);
-          k4[u][2] = __low2float(k23);
-          k4[u][3] = __high2float(k23);
+          kw[u] = *reinterpret_cast<const uint2*>(kr + 4 * lane);
+        }
+      }
+      float v[V];
+#pragma unroll
+      for (int u = 0; u < kRows; ++u) {
+        const __nv_bfloat162 k01 = *reinterpret_cast<const __nv_bfloat162*>(&kw[u].x);
+        const __nv_bfloat162 k23 = *reinterpret_cast<const __nv_bfloat162*>(&kw[u].y);
+        const float k0 = __low2float(k01), k1 = __high2float(k01), k2 = __low2float(k23), k3 = __high2float(k23);
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+          v[u * NR + j] = fmaf(Qr[j][0], k0, fmaf(Qr[j][1], k1, fmaf(Qr[j][2], k2, Qr[j][3] * k3)));
+      }
+      // reduce-scatter: after LV halving steps lane holds value idx = lane >> (5 - LV)
+#pragma unroll
+      for (int st2 = 0; st2 < LV; ++st2) {
+        const int o = 16 >> st2, half = V >> (st2 + 1);
+        const bool up = lane & o;
+#pragma unroll
+        for (int i2 = 0; i2 < half; ++i2) {
+          const float keep = up ? v[i2 + half] : v[i2], send = up ? v[i2] : v[i2 + half];
+          v[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
         }
       }
 #pragma unroll
-      for (int u = 0; u < kRows; ++u) {
-        const int it = it0 + u * kWarps;
+      for (int o = 16 >> LV; o; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+      const int idx = lane >> (5 - LV), u = idx / NR, j = idx - u * NR;
+      const int it = it0 + u * kWarps;
+      // the lane's row data: select from the unrolled arrays without local memory
+      int pos = -1;
+      bool spec = false;
 #pragma unroll
-        for (int j = 0; j < NR; ++j) {
-          float sv = fmaf(Qr[j][0], k4[u][0], fmaf(Qr[j][1], k4[u][1], fmaf(Qr[j][2], k4[u][2], Qr[j][3] * k4[u][3])));
-          sv = warp_sum_all(sv);
-          if (lane == j && it < count) {
-            const bool m = specr[u] && j < G.G;  // row 0 never sees the speculative column
-            ex.sc[j][it] = m ? -CUDART_INF_F : sv;
-            if (posr[u] >= 0 && j >= agg_j0 && j < agg_j0 + G.G)
-              a.spill[((size_t)b * G.Hq + h * G.G + (j - agg_j0)) * G.L + posr[u]] = sv;
-          }
+      for (int uu = 0; uu < kRows; ++uu)
+        if (uu == u) {
+          pos = posr[uu];
+          spec = specr[uu];
         }
+      if ((lane & ((1 << (5 - LV)) - 1)) == 0 && it < count) {
+        const float sv = v[0];
+        const bool m = spec && j < G.G;  // row 0 never sees the speculative column
+        ex.sc[j][it] = m ? -CUDART_INF_F : sv;
+        if (pos >= 0 && j >= agg_j0 && j < agg_j0 + G.G)
+          a.spill[((size_t)b * G.Hq + h * G.G + (j - agg_j0)) * G.L + pos] = sv;
       }
     }
     __syncthreads();
-    if (warp < NR) {  // online softmax of row `warp` over the chunk
+    if (warp < NR) {  // online softmax of row `warp` over the chunk + pinned-only stats
       const int j = warp;
-      float mx = -CUDART_INF_F;
-      for (int i = lane; i < count; i += 32) mx = fmaxf(mx, ex.sc[j][i]);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const float mold = ex.m[j], mnew = fmaxf(mold, mx);
-      float sum = 0.f;
+      const int npc = max(0, min(count, npin - c0));  // pinned rows in this chunk
+      float mx = -CUDART_INF_F, mxp = -CUDART_INF_F;
       for (int i = lane; i < count; i += 32) {
-        const float p = mnew == -CUDART_INF_F ? 0.f : fast_exp2(ex.sc[j][i] - mnew);
+        const float x = ex.sc[j][i];
+        mx = fmaxf(mx, x);
+        if (i < npc) mxp = fmaxf(mxp, x);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mxp = fmaxf(mxp, __shfl_xor_sync(0xffffffffu, mxp, o));
+      }
+      const float mold = ex.m[j], mnew = fmaxf(mold, mx);
+      const float pmold = ex.pm[j], pmnew = fmaxf(pmold, mxp);
+      float sum = 0.f, psum = 0.f;
+      for (int i = lane; i < count; i += 32) {
+        const float x = ex.sc[j][i];
+        const float p = mnew == -CUDART_INF_F ? 0.f : fast_exp2(x - mnew);
+        if (i < npc) psum += pmnew == -CUDART_INF_F ? 0.f : fast_exp2(x - pmnew);
         ex.sc[j][i] = p;
         sum += p;
       }
       sum = warp_sum_all(sum);
+      psum = warp_sum_all(psum);
       __syncwarp();
       if (lane == 0) {
         const float f = mold == -CUDART_INF_F ? 0.f : exp2f(mold - mnew);
         ex.fac[j] = f;
         ex.m[j] = mnew;
         ex.l[j] = ex.l[j] * f + sum;
+        const float pf = pmold == -CUDART_INF_F ? 0.f : exp2f(pmold - pmnew);
+        ex.pm[j] = pmnew;
+        ex.pl[j] = ex.pl[j] * pf + psum;
       }
     }
     __syncthreads();
@@ -359,47 +399,40 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
       acc[j][2] *= f;
       acc[j][3] *= f;
     }
+    // ---- P.V: kRows value rows per warp batch, loads first
     for (int it0 = warp; it0 < count; it0 += kWarps * kRows) {
-      float v4[kRows][4];
+      uint2 vwr[kRows];
 #pragma unroll
       for (int u = 0; u < kRows; ++u) {
         const int it = it0 + u * kWarps;
-        v4[u][0] = v4[u][1] = v4[u][2] = v4[u][3] = 0.f;
+        vwr[u] = make_uint2(0u, 0u);
         if (it < count) {
           const __nv_bfloat16 *kr, *vr;
           int pos;
           bool spec;
           row_ptr(c0 + it, kr, vr, pos, spec);
-          const uint2 w = *reinterpret_cast<const uint2*>(vr + 4 * lane);
-          const __nv_bfloat162 v01 = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
-          const __nv_bfloat162 v23 = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
-          v4[u][0] = __low2float(v01);
-          v4[u][1] = __high2float(v01);
-          v4[u][2] = __low2float(v23);
-          v4[u][3] = __high2float(v23);
+          vwr[u] = *reinterpret_cast<const uint2*>(vr + 4 * lane);
         }
       }
 #pragma unroll
       for (int u = 0; u < kRows; ++u) {
         const int it = it0 + u * kWarps;
         if (it < count) {
+          const __nv_bfloat162 v01 = *reinterpret_cast<const __nv_bfloat162*>(&vwr[u].x);
+          const __nv_bfloat162 v23 = *reinterpret_cast<const __nv_bfloat162*>(&vwr[u].y);
+          const float x0 = __low2float(v01), x1 = __high2float(v01), x2 = __low2float(v23), x3 = __high2float(v23);
 #pragma unroll
           for (int j = 0; j < NR; ++j) {
             const float p = ex.sc[j][it];
-            acc[j][0] = fmaf(p, v4[u][0], acc[j][0]);
-            acc[j][1] = fmaf(p, v4[u][1], acc[j][1]);
-            acc[j][2] = fmaf(p, v4[u][2], acc[j][2]);
-            acc[j][3] = fmaf(p, v4[u][3], acc[j][3]);
+            acc[j][0] = fmaf(p, x0, acc[j][0]);
+            acc[j][1] = fmaf(p, x1, acc[j][1]);
+            acc[j][2] = fmaf(p, x2, acc[j][2]);
+            acc[j][3] = fmaf(p, x3, acc[j][3]);
           }
         }
       }
     }
     __syncthreads();
-    if (cend == npin && tid < NR) {  // state after the pinned rows only
-      ex.pm[tid] = ex.m[tid];
-      ex.pl[tid] = ex.l[tid];
-    }
-    c0 = cend;
   }
 #pragma unroll
   for (int j = 0; j < NR; ++j)
