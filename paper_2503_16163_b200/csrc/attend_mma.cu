@@ -133,6 +133,12 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
@@ -192,9 +198,24 @@ struct MergeSmem {
   float l[kWarps][NR];
 };
 
-// exact segment scratch (split == nsplit CTAs)
+// exact segment scratch (split == nsplit CTAs): a chunk of CH full-precision
+// K and V rows is staged into shared memory with cp.async before any math
 template <int NR>
 struct ExactSmem {
+  static constexpr int CH = 128;  // (staged form: NR <= 4)
+  uint4 krow[CH][16];  // bf16 x 128 per row
+  uint4 vrow[CH][16];
+  float sc[NR][CH];
+  float fac[NR], m[NR], l[NR], pm[NR], pl[NR];
+  int slots[1024];     // occupied pin slots, slot order
+  int spos[1024];      // their positions
+  int npin;
+  float o[kWarps][NR][128];
+};
+
+// exact segment scratch, direct-load form
+template <int NR>
+struct ExactRowsSmem {
   static constexpr int CH = 512;
   float sc[NR][CH];
   float fac[NR], m[NR], l[NR], pm[NR], pl[NR];
@@ -206,11 +227,220 @@ struct ExactSmem {
 template <int BITS, int NR>
 constexpr size_t fast_smem_bytes() {
   size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps + (NR > 2 ? NR * 32 * 16 : 0), b = sizeof(MergeSmem<NR>),
-         c = sizeof(ExactSmem<NR>);
+         c = NR == 8 ? sizeof(ExactRowsSmem<NR>) : sizeof(ExactSmem<NR>);
   return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 
 // ---- exact segment: pinned slots + residual ring + in-step rows (bf16, exact) ----------
+// One CTA per (seq, kv head), 8 warps, latency-oriented.  Rows come in chunks
+// of CH: every K and V row of the chunk is staged into shared memory with
+// 16-byte cp.async copies issued up front (one memory round trip per chunk),
+// then a warp scores kRows rows per batch and finishes the NR x kRows per-lane
+// partial dot products with one warp reduce-scatter (V-1 shuffles).  Online
+// softmax across chunks; the pinned rows' own (max, sum) -- the pinned mass,
+// engine.py:314-316 -- is tracked alongside.
+template <int NR>
+__device__ void exact_segment_fast(const AttnArgs& a, const int split, const int h, const int b,
+                                   unsigned char* smem) {
+  const Geo& G = a.G;
+  const LayerBufs& B = a.B;
+  ExactSmem<NR>& ex = *reinterpret_cast<ExactSmem<NR>*>(smem);
+  constexpr int CH = ExactSmem<NR>::CH;
+  constexpr int kRows = NR <= 2 ? 4 : 16 / NR;  // rows per warp batch
+  constexpr int V = NR * kRows;                  // partial sums per lane per batch: 4, 8 or 16
+  constexpr int LV = V == 4 ? 2 : V == 8 ? 3 : 4;
+  static_assert(V == (1 << LV), "reduce-scatter needs a power-of-two value count");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int unit = G.scope ? h : 0, hh = G.scope ? 0 : h;
+  float Qr[NR][4];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const int r = j / G.G, g2 = j - r * G.G;
+    const uint2 w = *reinterpret_cast<const uint2*>(a.q + (((size_t)b * a.rows + r) * G.Hq + h * G.G + g2) * 128 + 4 * lane);
+    const __nv_bfloat162 q01 = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
+    const __nv_bfloat162 q23 = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
+    Qr[j][0] = __low2float(q01) * a.sm_scale_log2;
+    Qr[j][1] = __high2float(q01) * a.sm_scale_log2;
+    Qr[j][2] = __low2float(q23) * a.sm_scale_log2;
+    Qr[j][3] = __high2float(q23) * a.sm_scale_log2;
+  }
+  const int32_t* pp = B.pin_pos + ((size_t)b * G.U + unit) * G.k;
+  if (warp == 0) {  // ballot compaction of the occupied slots (and their positions), in slot order
+    int cnt = 0;
+    for (int s0 = 0; s0 < G.k; s0 += 32) {
+      const int pos = s0 + lane < G.k ? pp[s0 + lane] : -1;
+      const bool occ = pos >= 0;
+      const unsigned m = __ballot_sync(0xffffffffu, occ);
+      if (occ) {
+        const int w = cnt + __popc(m & ((1u << lane) - 1u));
+        ex.slots[w] = s0 + lane;
+        ex.spos[w] = pos;
+      }
+      cnt += __popc(m);
+    }
+    if (lane == 0) ex.npin = cnt;
+  }
+  if (tid < NR) {
+    ex.m[tid] = -CUDART_INF_F;
+    ex.l[tid] = 0.f;
+    ex.pm[tid] = -CUDART_INF_F;
+    ex.pl[tid] = 0.f;
+  }
+  __syncthreads();
+  const int npin = ex.npin, nres = a.n - a.f, total = npin + nres + a.rows;
+  const int agg_j0 = a.agg_row * G.G;
+  float acc[NR][4];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+
+  for (int c0 = 0; c0 < total; c0 += CH) {
+    const int count = min(total, c0 + CH) - c0;
+    // ---- stage the chunk: warp-sized groups of 32 x 16 B = one K row (lanes 0-15) + its V row
+    for (int i = tid; i < count * 32; i += kThreads) {
+      const int r = i >> 5, piece = i & 31, it = c0 + r;
+      const __nv_bfloat16* base;
+      if (it < npin) {
+        const size_t o = ((((size_t)b * G.U + unit) * G.k + ex.slots[it]) * G.Hu + hh) * 128;
+        base = (piece < 16 ? B.pool_k : B.pool_v) + o;
+      } else if (it < npin + nres) {
+        const int p = a.f + (it - npin);
+        const size_t o = (((size_t)b * G.H + h) * G.ring + p % G.ring) * 128;
+        base = (piece < 16 ? B.ring_k : B.ring_v) + o;
+      } else {
+        const size_t o = (((size_t)b * a.rows + (it - npin - nres)) * G.H + h) * 128;
+        base = (piece < 16 ? a.k_new : a.v_new) + o;
+      }
+      cp_async16(piece < 16 ? &ex.krow[r][piece] : &ex.vrow[r][piece - 16],
+                 reinterpret_cast<const uint4*>(base) + (piece & 15));
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- scores: kRows rows per warp batch, one reduce-scatter
+    for (int it0 = warp; it0 < count; it0 += kWarps * kRows) {
+      float v[V];
+#pragma unroll
+      for (int u = 0; u < kRows; ++u) {
+        const int it = min(it0 + u * kWarps, count - 1);  // rows past the chunk are discarded below
+        const uint2 kw = reinterpret_cast<const uint2*>(ex.krow[it])[lane];
+        const __nv_bfloat162 k01 = *reinterpret_cast<const __nv_bfloat162*>(&kw.x);
+        const __nv_bfloat162 k23 = *reinterpret_cast<const __nv_bfloat162*>(&kw.y);
+        const float k0 = __low2float(k01), k1 = __high2float(k01), k2 = __low2float(k23), k3 = __high2float(k23);
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+          v[u * NR + j] = fmaf(Qr[j][0], k0, fmaf(Qr[j][1], k1, fmaf(Qr[j][2], k2, Qr[j][3] * k3)));
+      }
+      // reduce-scatter: after LV halving steps lane holds value idx = lane >> (5 - LV)
+#pragma unroll
+      for (int st2 = 0; st2 < LV; ++st2) {
+        const int o = 16 >> st2, half = V >> (st2 + 1);
+        const bool up = lane & o;
+#pragma unroll
+        for (int i2 = 0; i2 < half; ++i2) {
+          const float keep = up ? v[i2 + half] : v[i2], send = up ? v[i2] : v[i2 + half];
+          v[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+#pragma unroll
+      for (int o = 16 >> LV; o; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+      const int idx = lane >> (5 - LV), u = idx / NR, j = idx - u * NR;
+      const int it = it0 + u * kWarps;
+      if ((lane & ((1 << (5 - LV)) - 1)) == 0 && it < count) {
+        const int g = c0 + it;  // row index over the whole segment
+        const float sv = v[0];
+        const bool m = (g == npin + nres + 1) && j < G.G;  // row 0 never sees the speculative column
+        ex.sc[j][it] = m ? -CUDART_INF_F : sv;
+        if (g < npin && j >= agg_j0 && j < agg_j0 + G.G)
+          a.spill[((size_t)b * G.Hq + h * G.G + (j - agg_j0)) * G.L + ex.spos[g]] = sv;
+      }
+    }
+    __syncthreads();
+    if (warp < NR) {  // online softmax of row `warp` over the chunk + pinned-only stats
+      const int j = warp;
+      const int npc = max(0, min(count, npin - c0));  // pinned rows in this chunk
+      float mx = -CUDART_INF_F, mxp = -CUDART_INF_F;
+      for (int i = lane; i < count; i += 32) {
+        const float x = ex.sc[j][i];
+        mx = fmaxf(mx, x);
+        if (i < npc) mxp = fmaxf(mxp, x);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mxp = fmaxf(mxp, __shfl_xor_sync(0xffffffffu, mxp, o));
+      }
+      const float mold = ex.m[j], mnew = fmaxf(mold, mx);
+      const float pmold = ex.pm[j], pmnew = fmaxf(pmold, mxp);
+      float sum = 0.f, psum = 0.f;
+      for (int i = lane; i < count; i += 32) {
+        const float x = ex.sc[j][i];
+        const float p = mnew == -CUDART_INF_F ? 0.f : fast_exp2(x - mnew);
+        if (i < npc) psum += pmnew == -CUDART_INF_F ? 0.f : fast_exp2(x - pmnew);
+        ex.sc[j][i] = p;
+        sum += p;
+      }
+      sum = warp_sum_all(sum);
+      psum = warp_sum_all(psum);
+      __syncwarp();
+      if (lane == 0) {
+        const float f = mold == -CUDART_INF_F ? 0.f : exp2f(mold - mnew);
+        ex.fac[j] = f;
+        ex.m[j] = mnew;
+        ex.l[j] = ex.l[j] * f + sum;
+        const float pf = pmold == -CUDART_INF_F ? 0.f : exp2f(pmold - pmnew);
+        ex.pm[j] = pmnew;
+        ex.pl[j] = ex.pl[j] * pf + psum;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const float f = ex.fac[j];
+      acc[j][0] *= f;
+      acc[j][1] *= f;
+      acc[j][2] *= f;
+      acc[j][3] *= f;
+    }
+    // ---- P.V from the staged value rows
+    for (int it = warp; it < count; it += kWarps) {
+      const uint2 vw = reinterpret_cast<const uint2*>(ex.vrow[it])[lane];
+      const __nv_bfloat162 v01 = *reinterpret_cast<const __nv_bfloat162*>(&vw.x);
+      const __nv_bfloat162 v23 = *reinterpret_cast<const __nv_bfloat162*>(&vw.y);
+      const float x0 = __low2float(v01), x1 = __high2float(v01), x2 = __low2float(v23), x3 = __high2float(v23);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const float p = ex.sc[j][it];
+        acc[j][0] = fmaf(p, x0, acc[j][0]);
+        acc[j][1] = fmaf(p, x1, acc[j][1]);
+        acc[j][2] = fmaf(p, x2, acc[j][2]);
+        acc[j][3] = fmaf(p, x3, acc[j][3]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < NR; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ex.o[warp][j][4 * lane + i] = acc[j][i];
+  __syncthreads();
+  const size_t base = (((size_t)b * G.H + h) * (a.nsplit + 1) + split) * NR;
+  for (int i = tid; i < NR * 128; i += kThreads) {
+    const int j = i >> 7, c = i & 127;
+    float o = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) o += ex.o[w][j][c];
+    a.part_o[(base + j) * 128 + c] = o;
+  }
+  if (tid < NR) {
+    a.part_ml[(base + tid) * 2 + 0] = ex.m[tid];
+    a.part_ml[(base + tid) * 2 + 1] = ex.l[tid];
+    const size_t pb = ((size_t)b * G.H + h) * NR + tid;
+    a.pin_ml[pb * 2 + 0] = ex.pm[tid];
+    a.pin_ml[pb * 2 + 1] = ex.pl[tid];
+  }
+}
+
+// ---- exact segment, direct-load form (used for NR = 8, where overlapping the row loads
+// with the 8-row dot products beats staging) ----------------------------------------
 // One CTA per (seq, kv head), 8 warps, latency-oriented: a warp scores kRows
 // rows per batch with every row's 8-byte key load issued before any math, and
 // the NR x kRows per-lane partial dot products are finished by one warp
@@ -219,12 +449,12 @@ constexpr size_t fast_smem_bytes() {
 // (max, sum) -- the pinned mass, engine.py:314-316 -- is tracked alongside, so
 // pinned and residual rows share one chunk.
 template <int NR>
-__device__ void exact_segment_fast(const AttnArgs& a, const int split, const int h, const int b,
+__device__ void exact_segment_rows(const AttnArgs& a, const int split, const int h, const int b,
                                    unsigned char* smem) {
   const Geo& G = a.G;
   const LayerBufs& B = a.B;
-  ExactSmem<NR>& ex = *reinterpret_cast<ExactSmem<NR>*>(smem);
-  constexpr int CH = ExactSmem<NR>::CH;
+  ExactRowsSmem<NR>& ex = *reinterpret_cast<ExactRowsSmem<NR>*>(smem);
+  constexpr int CH = ExactRowsSmem<NR>::CH;
   constexpr int kRows = NR <= 2 ? 4 : 16 / NR;  // rows per warp batch (measured best; NR=8 spill-free)
   constexpr int V = NR * kRows;                  // partial sums per lane per batch: 4, 8 or 16
   constexpr int LV = V == 4 ? 2 : V == 8 ? 3 : 4;
@@ -470,7 +700,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (split == a.nsplit) {
-    exact_segment_fast<NR>(a, split, h, b, smem_raw);
+    if constexpr (NR == 8) exact_segment_rows<NR>(a, split, h, b, smem_raw);
+    else exact_segment_fast<NR>(a, split, h, b, smem_raw);
     return;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
