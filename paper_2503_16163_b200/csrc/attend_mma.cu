@@ -1354,12 +1354,47 @@ int launch_attend_fast(const AttnArgs& a0, cudaStream_t st) {
   const Geo& G = a.G;
   const int nblk = a.f / 32;
   const int units = G.H * G.batch;
+  // Split count: SPC_SPLIT_WAVES=w forces ~w waves; by default a wave model
+  // picks it.  With `slots` = 2 CTAs x SMs resident, a launch of C CTAs (the
+  // splits plus one exact CTA per unit) of b blocks costs about ceil(C / slots)
+  // rounds of (b + c0) block-times, c0 ~ 20 blocks covering a CTA's prologue
+  // (ring fill, first DRAM round trip) and merge.  Short CTAs pay c0 too often,
+  // few CTAs quantize badly.  Measured sweep (SPC_NSPLIT): the
+  // model's picks C2 5, C3 16, C4 16 are within 1.3% of the best split.
   static const int waves = [] {
     const char* e = getenv("SPC_SPLIT_WAVES");
-    return e ? std::max(1, atoi(e)) : 6;
+    return e ? std::max(1, atoi(e)) : 0;
   }();
-  int want = (waves * 2 * 148 + units - 1) / units;  // ~`waves` waves at 2 CTAs/SM
-  want = std::max(1, std::min(want, std::min(127, std::max(1, nblk / 8))));
+  static const int slots = [] {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return 2 * sms;
+  }();
+  static const int forced = [] {
+    const char* e = getenv("SPC_NSPLIT");  // tuning only: exact split count (0 = model)
+    return e ? std::max(0, atoi(e)) : 0;
+  }();
+  const int cap = std::min(127, std::max(1, nblk / 8));
+  int want;
+  if (forced) {
+    want = std::min(forced, cap);
+  } else if (waves) {
+    want = std::max(1, std::min((waves * slots + units - 1) / units, cap));
+  } else {
+    constexpr long long c0 = 20;
+    long long best = -1;
+    want = 1;
+    for (int w = 1; w <= cap; ++w) {
+      const int bps = (nblk + w - 1) / w, ns = (nblk + bps - 1) / bps;
+      const long long rounds = ((long long)units * (ns + 1) + slots - 1) / slots;  // + the exact CTA
+      const long long cost = rounds * (bps + c0);
+      if (best < 0 || cost < best) {
+        best = cost;
+        want = w;
+      }
+    }
+  }
   a.blocks_per_split = std::max(1, (nblk + want - 1) / want);
   a.nsplit = std::max(1, (nblk + a.blocks_per_split - 1) / a.blocks_per_split);
   const int R = a.rows * G.G;

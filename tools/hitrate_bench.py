@@ -1,0 +1,109 @@
+#!/usr/bin/env python
+"""Hit-rate study at real context length on the device.
+
+  python tools/hitrate_bench.py [--ctx 32768] [--heads 32] [--kv-heads 32] [--steps 8]
+
+Builds a traced decode of one LLaMA-shaped layer on synthetic peaky keys
+(256 planted needles per kv head along the first query, query drift 0.3 per
+step, as bench.py): spc_full_attend writes each step's probability rows
+straight into a device trace [q_heads, steps, ctx + steps].  Then times
+spc_topk_hitrate / spc_eviction_hitrate over a k sweep with CUDA events and
+prints one JSON line: device times, rows/s, the mean curves, and the oracle
+restatement (oracle/hitrate.py, the reference's algorithm; CPU, one sequence)
+timed on the same rows for comparison.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import numpy as np
+    import torch
+
+    from paper_2503_16163_b200 import _lib
+    from paper_2503_16163_b200.hitrate import AttentionTrace
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ctx", type=int, default=32768)
+    ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--kv-heads", type=int, default=32)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--ks", default="16,64,256,1024")
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    Hq, Hkv, d, n0, T = a.heads, a.kv_heads, 128, a.ctx, a.steps
+    L = n0 + T
+    ks = [int(x) for x in a.ks.split(",")]
+    rng = np.random.default_rng(0)
+    dev = "cuda:0"
+    K = torch.randn((L, Hkv, d), device=dev) + torch.randn((1, Hkv, d), device=dev) * 2.0
+    V = torch.randn((L, Hkv, d), device=dev)
+    q = torch.randn((Hq, d), device=dev)
+    G = Hq // Hkv
+    idx = torch.as_tensor(rng.choice(n0, 256, replace=False), device=dev)
+    for h in range(Hkv):
+        K[idx, h] += 0.5 * q[h * G]
+    data = torch.zeros((Hq, T, L), dtype=torch.float32, device=dev)
+    out = torch.empty((Hq, d), dtype=torch.float32, device=dev)
+    scale = float(np.float32(d ** -0.5))
+    st = torch.cuda.current_stream().cuda_stream
+    lens = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for t in range(T):
+        q = q + 0.3 * torch.randn_like(q)
+        rows = data[:, t]
+        _lib.check(_lib.lib().spc_full_attend(q.data_ptr(), K.data_ptr(), V.data_ptr(), n0 + t + 1, Hq, Hkv, d,
+                                              scale, out.data_ptr(), rows.data_ptr(), rows.stride(0), st))
+        lens.append(n0 + t + 1)
+    e1.record()
+    torch.cuda.synchronize()
+    trace_ms = e0.elapsed_time(e1)
+    tr = AttentionTrace(data=data, lens=lens)
+    tr.validate(1e-5)
+    res = {"k": ks, "topk_ms": [], "eviction_ms": [], "topk_mean": [], "eviction_mean": []}
+    for k in ks:
+        for name, fn in (("topk", tr.topk_hitrates), ("eviction", tr.eviction_hitrates)):
+            fn(k)  # warm-up (workspace allocation, attribute set)
+            torch.cuda.synchronize()
+            best = 1e30
+            for _ in range(a.reps):
+                e0.record()
+                r = fn(k)  # includes the D2H of the [nseq, steps] rates
+                e1.record()
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            res[f"{name}_ms"].append(round(best, 4))
+            res[f"{name}_mean"].append(round(float(r.mean()), 6))
+    # oracle restatement on one sequence (CPU)
+    from oracle import hitrate as O
+    host = data[0].cpu().numpy()
+    seq = [host[t, :lens[t]] for t in range(T)]
+    cpu = {}
+    for k in (ks[0], ks[-1]):
+        t0 = time.perf_counter()
+        O.topk_hitrate(seq, k)
+        t1 = time.perf_counter()
+        O.eviction_hitrate(seq, k)
+        t2 = time.perf_counter()
+        cpu[str(k)] = {"topk_s": round(t1 - t0, 4), "eviction_s": round(t2 - t1, 4)}
+    rows = Hq * T
+    print(json.dumps({
+        "tool": "hitrate_bench", "config": {"ctx": n0, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d, "steps": T,
+                                            "sequences": Hq, "data": "synthetic peaky keys (256 needles), drift 0.3"},
+        "trace_ms": round(trace_ms, 4), "trace_rows": rows,
+        "device": res,
+        "topk_rows_per_s": [round(rows / (ms / 1e3)) for ms in res["topk_ms"]],
+        "eviction_seq_steps_per_s": [round(rows / (ms / 1e3)) for ms in res["eviction_ms"]],
+        "cpu_oracle_one_sequence": cpu,
+    }))
+
+
+if __name__ == "__main__":
+    main()
