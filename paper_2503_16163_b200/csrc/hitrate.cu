@@ -5,7 +5,7 @@
 //
 //   spc_full_attend       exact fp32 attention of one decode step over a full
 //                         cache, writing the per-q-head probability rows into a
-//                         trace                                engine.py:51-63
+//                         trace (3 chunked passes)             engine.py:51-63
 //   spc_trace_row_sums    np.sum(row) of every trace row (float32 pairwise),
 //                         the AttentionTrace.validate check   hitrate.py:27-31
 //   spc_topk_hitrate      mass of the k largest entries of each row
@@ -171,20 +171,27 @@ __device__ __forceinline__ uint64_t ord64(double x) {
 }
 
 // ---- exact fp32 attention of one step (engine.py:51-63) --------------------------------
-// grid = q heads; a warp scores one key row at a time (lanes over channels)
-__global__ void __launch_bounds__(kT) k_full_attend(const float* __restrict__ q, const float* __restrict__ K,
-                                                    const float* __restrict__ V, int n, int group, int Hkv, int d,
-                                                    float scale, float* __restrict__ out, float* __restrict__ probs,
-                                                    int64_t probs_ld) {
-  const int hq = blockIdx.x, hk = hq / group;
+// Three passes over position chunks of kFaChunk, grid (chunks, q heads) each, so a
+// 32k-position row spreads over the whole GPU:
+//   1. scores s_i = (q . k_i) * scale into the trace row (a warp per key row,
+//      lanes over channels, coalesced) + the chunk max;
+//   2. e_i = exp(s_i - M) with M the row max, the chunk sum, and the chunk's
+//      partial P.V (thread per channel, rows of the chunk);
+//   3. p_i = e_i / L with L the float64 sum of the chunk sums rounded to fp32
+//      (masked_softmax_rows, numerics.py:24-39), and out = sum(partials) / L.
+constexpr int kFaChunk = 1024;
+
+__global__ void __launch_bounds__(kT) k_fa_scores(const float* __restrict__ q, const float* __restrict__ K, int n,
+                                                  int group, int Hkv, int d, float scale, float* __restrict__ probs,
+                                                  int64_t probs_ld, float* __restrict__ cmax, int nchunk) {
+  const int chunk = blockIdx.x, hq = blockIdx.y, hk = hq / group;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* p = probs + (int64_t)hq * probs_ld;
   const float* qh = q + (size_t)hq * d;
   __shared__ float red[kT / 32];
-  __shared__ double dred[kT / 32];
-  __shared__ float bc;
+  const int i0 = chunk * kFaChunk, i1 = min(n, i0 + kFaChunk);
   float mx = -INFINITY;
-  for (int i = warp; i < n; i += kT / 32) {
+  for (int i = i0 + warp; i < i1; i += kT / 32) {
     const float* kr = K + ((size_t)i * Hkv + hk) * d;
     float s = 0.f;
     for (int c = lane; c < d; c += 32) s = fmaf(qh[c], kr[c], s);
@@ -199,42 +206,79 @@ __global__ void __launch_bounds__(kT) k_full_attend(const float* __restrict__ q,
   if (threadIdx.x == 0) {
     float m = red[0];
     for (int w = 1; w < kT / 32; ++w) m = fmaxf(m, red[w]);
-    bc = m;
+    cmax[(size_t)hq * nchunk + chunk] = m;
+  }
+}
+
+__global__ void __launch_bounds__(kT) k_fa_exp(const float* __restrict__ V, int n, int group, int Hkv, int d,
+                                               float* __restrict__ probs, int64_t probs_ld,
+                                               const float* __restrict__ cmax, double* __restrict__ csum,
+                                               float* __restrict__ opart, int nchunk) {
+  const int chunk = blockIdx.x, hq = blockIdx.y, hk = hq / group;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* p = probs + (int64_t)hq * probs_ld;
+  __shared__ float sM;
+  __shared__ double dred[kT / 32];
+  __shared__ float part[kT];
+  if (threadIdx.x < 32) {
+    float m = -INFINITY;
+    for (int c = lane; c < nchunk; c += 32) m = fmaxf(m, cmax[(size_t)hq * nchunk + c]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) sM = m;
   }
   __syncthreads();
-  const float m = bc;
+  const float M = sM;
+  const int i0 = chunk * kFaChunk, i1 = min(n, i0 + kFaChunk);
   double sum = 0.0;
-  for (int i = threadIdx.x; i < n; i += kT) {
-    const float e = expf(p[i] - m);
+  for (int i = i0 + threadIdx.x; i < i1; i += kT) {
+    const float e = expf(p[i] - M);
     p[i] = e;
     sum += (double)e;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   if (lane == 0) dred[warp] = sum;
-  __syncthreads();
+  __syncthreads();  // also orders this CTA's e_i writes before the P.V reads below
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < kT / 32; ++w) s += dred[w];
-    bc = (float)s;
+    csum[(size_t)hq * nchunk + chunk] = s;
   }
-  __syncthreads();
-  const float tot = bc;
-  for (int i = threadIdx.x; i < n; i += kT) p[i] = p[i] / tot;
-  __syncthreads();
-  // out[c] = sum_i p_i V[i, c]: channel-parallel, rows split over kT/d thread groups
-  __shared__ float part[kT];
   const int per = d <= kT ? kT / d : 1;
   const int c = threadIdx.x % d, grp = threadIdx.x / d;
   float acc = 0.f;
   if (threadIdx.x < per * d)
-    for (int i = grp; i < n; i += per) acc = fmaf(p[i], V[((size_t)i * Hkv + hk) * d + c], acc);
+    for (int i = i0 + grp; i < i1; i += per) acc = fmaf(p[i], V[((size_t)i * Hkv + hk) * d + c], acc);
   part[threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.x < d) {
     float o = 0.f;
     for (int g2 = 0; g2 < per; ++g2) o += part[g2 * d + threadIdx.x];
-    out[(size_t)hq * d + threadIdx.x] = o;
+    opart[((size_t)hq * nchunk + chunk) * d + threadIdx.x] = o;
+  }
+}
+
+__global__ void __launch_bounds__(kT) k_fa_finish(int n, int d, float* __restrict__ probs, int64_t probs_ld,
+                                                  const double* __restrict__ csum,
+                                                  const float* __restrict__ opart, float* __restrict__ out,
+                                                  int nchunk) {
+  const int chunk = blockIdx.x, hq = blockIdx.y;
+  float* p = probs + (int64_t)hq * probs_ld;
+  __shared__ float sL;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int c = 0; c < nchunk; ++c) s += csum[(size_t)hq * nchunk + c];
+    sL = (float)s;
+  }
+  __syncthreads();
+  const float L = sL;
+  const int i0 = chunk * kFaChunk, i1 = min(n, i0 + kFaChunk);
+  for (int i = i0 + threadIdx.x; i < i1; i += kT) p[i] = p[i] / L;
+  if (chunk == 0 && threadIdx.x < d) {
+    float o = 0.f;
+    for (int c = 0; c < nchunk; ++c) o += opart[((size_t)hq * nchunk + c) * d + threadIdx.x];
+    out[(size_t)hq * d + threadIdx.x] = o / L;
   }
 }
 
@@ -469,9 +513,24 @@ int spc_full_attend(const float* q, const float* k, const float* v, int n, int q
   if (q_heads <= 0 || kv_heads <= 0 || q_heads % kv_heads) return bad("q_heads must be a multiple of kv_heads");
   if (head_dim <= 0 || head_dim > kT) return bad("full_attend: head_dim must be in [1, 256]");
   if (probs_ld < n) return bad("full_attend: probs_ld < n");
-  k_full_attend<<<q_heads, kT, 0, (cudaStream_t)stream>>>(q, k, v, n, q_heads / kv_heads, kv_heads, head_dim,
-                                                          scale, out, probs, probs_ld);
-  return cuda_status(cudaGetLastError());
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nchunk = (n + kFaChunk - 1) / kFaChunk;
+  const size_t nst = (size_t)q_heads * nchunk;
+  char* ws = nullptr;
+  if (cudaMallocAsync((void**)&ws, nst * (sizeof(float) + sizeof(double) + (size_t)head_dim * sizeof(float)), st) !=
+      cudaSuccess)
+    return spc::set_error(SPC_ENOMEM, "full_attend workspace");
+  double* csum = reinterpret_cast<double*>(ws);
+  float* cmax = reinterpret_cast<float*>(csum + nst);
+  float* opart = cmax + nst;
+  const dim3 grid(nchunk, q_heads);
+  const int group = q_heads / kv_heads;
+  k_fa_scores<<<grid, kT, 0, st>>>(q, k, n, group, kv_heads, head_dim, scale, probs, probs_ld, cmax, nchunk);
+  k_fa_exp<<<grid, kT, 0, st>>>(v, n, group, kv_heads, head_dim, probs, probs_ld, cmax, csum, opart, nchunk);
+  k_fa_finish<<<grid, kT, 0, st>>>(n, head_dim, probs, probs_ld, csum, opart, out, nchunk);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(ws, st);
+  return cuda_status(e);
 }
 
 int spc_trace_row_sums(const float* rows, int64_t seq_ld, int64_t row_ld, const int32_t* lens, int nseq, int steps,
