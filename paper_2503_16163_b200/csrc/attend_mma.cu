@@ -179,13 +179,14 @@ struct __align__(16) WarpSmem {
   static constexpr int kBkRow = 4 * NR + ((NR & 1) ? 0 : 4);
   uint4 bk[8][kBkRow];
   uint32_t stage[kStages][StageLayout<BITS>::words];      // TMA ring
-  // block probabilities: PG (<= 2 rows) [row][33]; otherwise [row & 1][token][row >> 1]
+  // block probabilities: PG (<= 2 rows) [row][40]; otherwise [row & 1][token][row >> 1]
   // in 132-float planes, conflict-free for both the score-side stores (t = c+gq,
   // row = 2tq+e) and the value-side loads (row = gq, t = c+2tq)
-  static constexpr int kPWords = NR * 4 <= 8 ? NR * 33 : 2 * 132;
+  // PG rows use stride 40 (even: token pairs load as float2; banks 8*row + t)
+  static constexpr int kPWords = NR * 4 <= 8 ? NR * 40 : 2 * 132;
   float P[kPWords];
   __device__ static constexpr int pidx(int row, int t) {
-    return NR * 4 <= 8 ? row * 33 + t : (row & 1) * 132 + t * 4 + (row >> 1);
+    return NR * 4 <= 8 ? row * 40 + t : (row & 1) * 132 + t * 4 + (row >> 1);
   }
   float4 sz[64];                                          // value (s*2^-q, z) pairs, vparams order
   uint64_t bar[kStages];
@@ -722,6 +723,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
     mbar_expect_tx(&ws.bar[st], SL::bytes);  // the whole block record, one bulk copy
     tma_load(s, rec_base + (size_t)blk * SL::words, SL::bytes, &ws.bar[st]);
   };
+  if constexpr (PACK && NR == 2) {  // bk padding columns 4*NR.. are the zero rows of the PACK B fragment
+    static_assert(WarpSmem<BITS, NR>::kBkRow >= 4 * NR + 4, "PACK zero padding");
+    ws.bk[lane >> 2][4 * NR + (lane & 3)] = make_uint4(0u, 0u, 0u, 0u);
+  }
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(&ws.bar[s], 1);
@@ -922,7 +927,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
       uint32_t b0, b1, b2 = 0, b3 = 0;
       if (PACK) {  // column n = gq = 2*row + plane; rows >= NR are zero columns
         uint2 bb = make_uint2(0, 0);
-        if ((gq >> 1) < NR) bb = reinterpret_cast<const uint2*>(&ws.bk[ks][4 * (gq >> 1) + (tq ^ ((ks >> 1) & 3))])[gq & 1];
+        if constexpr (NR == 2) {  // rows >= NR read the zeroed padding of bk (no predicate, no zeroing)
+          bb = reinterpret_cast<const uint2*>(&ws.bk[ks][4 * min(gq >> 1, NR) + (tq ^ ((ks >> 1) & 3))])[gq & 1];
+        } else if ((gq >> 1) < NR) {
+          bb = reinterpret_cast<const uint2*>(&ws.bk[ks][4 * (gq >> 1) + (tq ^ ((ks >> 1) & 3))])[gq & 1];
+        }
         b0 = bb.x;
         b1 = bb.y;
       } else {
@@ -1105,11 +1114,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
         const float4 sz1 = ws.sz[16 * grp + 4 * tq + 2 * ks + 1];
         const float spr4[4] = {sz0.x, sz0.z, sz1.x, sz1.z}, zz4[4] = {sz0.y, sz0.w, sz1.y, sz1.w};
         float x[4];
+        // P of tokens (t0, t0+1) and (t0+8, t0+9): two 8-byte loads
+        const int t0 = 16 * ks + 2 * tq;
+        float2 p01 = *reinterpret_cast<const float2*>(&ws.P[WarpSmem<BITS, NR>::pidx(prow, t0)]);
+        float2 p89 = *reinterpret_cast<const float2*>(&ws.P[WarpSmem<BITS, NR>::pidx(prow, t0 + 8)]);
+        if (!live) p01 = p89 = make_float2(0.f, 0.f);
+        const float pv[4] = {p01.x, p01.y, p89.x, p89.y};
 #pragma unroll
         for (int slot = 0; slot < 4; ++slot) {
-          const int khalf = slot >> 1;
-          const int t = 16 * ks + 2 * tq + (slot & 1) + 8 * khalf;
-          const float p = live ? ws.P[WarpSmem<BITS, NR>::pidx(prow, t)] : 0.f;
+          const float p = pv[slot];
           zacc[gi] = fmaf(p, zz4[slot], zacc[gi]);
           x[slot] = p * spr4[slot];
         }
