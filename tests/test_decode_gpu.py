@@ -163,6 +163,17 @@ def test_kv_head_scope_vs_oracle():
     _oracle_run((2, 1200, 4, 16, 128, 1, 32, 64, 16, "kv_head"), seed=21)
 
 
+def test_many_pins_multi_chunk_exact_segment():
+    """k=200 pins + residual > 128 rows: the staged exact segment (NR <= 4)
+    runs three chunks, with the pinned-only stats crossing chunk borders."""
+    _oracle_run((1, 3000, 4, 4, 128, 2, 32, 64, 200, "layer"), seed=31)
+
+
+def test_gqa_large_k_direct_exact_segment():
+    """C4-like: GQA-4 (8 rows, direct-load exact segment), 1-bit, k=256."""
+    _oracle_run((2, 3000, 2, 8, 128, 1, 32, 64, 256, "layer"), seed=32)
+
+
 def test_select_topk_kats_and_ties():
     from paper_2503_16163_b200 import select_topk
     assert select_topk([0.1, 0.9, 0.5], 2) == (1, 2)
