@@ -1160,32 +1160,43 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
     } else {
     // ---- value B fragments (f16 hi + lo: sum_t P*z and sum_t P*s*code may nearly cancel)
     // PG: lane column n = gq -> (grp = gq / NR, row = gq % NR); else row = gq, per group
-    uint32_t vb[PG ? 1 : 4][2][4];  // [grp][ks] {b0hi, b1hi, b0lo, b1lo}
-#pragma unroll
-    for (int gi = 0; gi < (PG ? 1 : 4); ++gi) {
-      const int grp = PG ? ((gq / NR) & 3) : gi;
-      const int row = PG ? (gq % NR) : gq;
-      const bool live = PG ? (gq < 4 * NR) : (gq < NR);
+    // Token-outer order: the lane's P values of a k-step (and P * token scale,
+    // P / 4 for the 1-bit zero point z = lo + (hi - lo) / 4) are formed once and
+    // shared by the four groups; per group and token only lo, hi, hi - lo and
+    // two products remain.
+    uint32_t vb[4][2][4];  // [grp][ks] {b0hi, b1hi, b0lo, b1lo}
+    {
+      const int row = gq;
+      const bool live = gq < NR;
       const int prow = row < NR ? row : 0;
-      const uint4 v0 = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * grp + 8 * tq);
-      const uint4 v1 = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * grp + 8 * tq + 4);
-      const uint32_t vpw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};  // [ks][slot]
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
-        float x[4];
+        float p[4], pv[4], p4[4];
 #pragma unroll
         for (int slot = 0; slot < 4; ++slot) {
           const int khalf = slot >> 1;
           const int t = 16 * ks + 2 * tq + (slot & 1) + 8 * khalf;
-          const uint32_t w = vpw[4 * ks + slot];
-          const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xFFFF0000u);
-          const float p = live ? ws.P[WarpSmem<BITS, NR>::pidx(prow, t)] : 0.f;
-          const float z = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
-          zacc[gi] = fmaf(p, z, zacc[gi]);
-          x[slot] = p * (hi - lo) * vscale[2 * ks + khalf];
+          p[slot] = live ? ws.P[WarpSmem<BITS, NR>::pidx(prow, t)] : 0.f;
+          pv[slot] = p[slot] * vscale[2 * ks + khalf];
+          p4[slot] = 0.25f * p[slot];
         }
-        split2(x[0], x[1], vb[gi][ks][0], vb[gi][ks][2]);
-        split2(x[2], x[3], vb[gi][ks][1], vb[gi][ks][3]);
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          // (lo | hi) words of tokens 16ks + 2tq + {0,1,8,9} of group gi
+          const uint4 vq = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * gi + 8 * tq + 4 * ks);
+          const uint32_t w4[4] = {vq.x, vq.y, vq.z, vq.w};
+          float x[4];
+#pragma unroll
+          for (int slot = 0; slot < 4; ++slot) {
+            const float lo = __uint_as_float(w4[slot] << 16), hi = __uint_as_float(w4[slot] & 0xFFFF0000u);
+            const float dd = hi - lo;
+            x[slot] = pv[slot] * dd;
+            zacc[gi] = fmaf(p[slot], lo, zacc[gi]);                  // sum_t P * lo
+            if (BITS == 1) zacc[gi] = fmaf(p4[slot], dd, zacc[gi]);  // + sum_t P * (hi - lo) / 4
+          }
+          split2(x[0], x[1], vb[gi][ks][0], vb[gi][ks][2]);
+          split2(x[2], x[3], vb[gi][ks][1], vb[gi][ks][3]);
+        }
       }
     }
     // value codes of this lane
