@@ -4,6 +4,8 @@
 // Reference: quant.py:59-190 (params, codes, LSB-first packing, per-channel key
 // groups, per-token value groups), kvcache.py:173-192 (migrate_residual),
 // kvcache.py:222-243 (materialize), kvcache.py:270-281 (snapshot).
+#include <math_constants.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -115,6 +117,192 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
   }
 }
 
+// Fast-layout quantizer (d = 128, g = 32, 1 or 2 bits): one CTA per g-token
+// block of one (seq, kv head), 256 threads, and every output word built in
+// registers by the thread that owns it -- no shared-memory atomics.
+//  * rows are staged with 16-byte loads into padded fp32 tiles;
+//  * threads 0..127 reduce a key group (one channel over the 32 tokens),
+//    threads 128..255 a value group (32 channels of one token);
+//  * codes: 1-bit is x >= thr where thr is the smallest fp32 >= the reference's
+//    float64 threshold zero + scale/2 (quant.py:81-84), so the fp32 compare is
+//    exact.  2-bit evaluates q ~= (x - z) / s in fp32 (error < 1.2e-6 on [0, 3])
+//    and takes rint/clip from it unless q lies within 1e-5 of a rounding
+//    boundary 0.5 / 1.5 / 2.5; those few elements (and degenerate scales) go
+//    through the reference's float64 division (quantize_code) -- bit-exact
+//    codes at fp32 cost.
+//  * key words are token-major rows (kloc), value words the MMA-fragment
+//    permutation (vloc), inverted here so each thread knows which (t, c) each
+//    of its word's bit fields holds.
+template <int BITS>
+__global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, QuantSrc S, int blk0) {
+  // tile rows padded so both code-word passes read shared memory conflict-free:
+  // key words (lanes = 4 tokens x 8 channel runs, rotated start) want LD = 1 mod 32,
+  // value words (lanes = tokens 2tq.. x channels gq) want LD = 4 mod 32
+  constexpr int g = 32, d = 128, LDK = 129, LDV = 132;
+  const int blk = blk0 + blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
+  __shared__ float xk[g * LDK];
+  __shared__ float xv[g * LDV];
+  __shared__ float kz[d], krs[d], kthr[d];     // key groups (fp32 fast-path data)
+  __shared__ double kz64[d], ks64[d];
+  __shared__ float vz[g * 4], vrs[g * 4], vthr[g * 4];
+  __shared__ double vz64[g * 4], vs64[g * 4];
+  __shared__ float s_rk, s_rv;
+  // ---- stage: 32 rows x 16 chunks of 16 bytes, for K and V
+  for (int i = tid; i < g * 16; i += 256) {
+    const int t = i >> 4, ch = i & 15;
+    const long long pos = (long long)blk * g + t;
+    const long long row = S.ring ? pos % S.ring : pos;
+    const long long off = b * S.seq_stride + row * S.tok_stride + (long long)h * S.head_stride + ch * 8;
+    const uint4 wk = *reinterpret_cast<const uint4*>(S.k + off);
+    const uint4 wv = *reinterpret_cast<const uint4*>(S.v + off);
+    const uint32_t ak[4] = {wk.x, wk.y, wk.z, wk.w}, av[4] = {wv.x, wv.y, wv.z, wv.w};
+    float* dk = xk + t * LDK + ch * 8;
+    float* dv = xv + t * LDV + ch * 8;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      dk[2 * e] = __uint_as_float(ak[e] << 16);
+      dk[2 * e + 1] = __uint_as_float(ak[e] & 0xFFFF0000u);
+      dv[2 * e] = __uint_as_float(av[e] << 16);
+      dv[2 * e + 1] = __uint_as_float(av[e] & 0xFFFF0000u);
+    }
+  }
+  if (tid == 0) {
+    s_rk = 0.f;
+    s_rv = 0.f;
+  }
+  __syncthreads();
+  const size_t bi = blk_index(G, b, h, blk);
+  // ---- group parameters
+  {
+    float lo, hi;
+    int gidx;
+    const bool key = tid < 128;
+    if (key) {  // key group: channel c over the block's tokens (quant.py:163-169)
+      const int c = tid;
+      lo = hi = xk[c];
+      for (int t = 1; t < g; ++t) {
+        const float x = xk[t * LDK + c];
+        lo = fminf(lo, x);
+        hi = fmaxf(hi, x);
+      }
+      B.kparams[bi * G.rec + kpi(G, c)] = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+      atomicMax(reinterpret_cast<unsigned*>(&s_rk), __float_as_uint(hi - lo));
+      gidx = c;
+    } else {    // value group: 32 channels of token t (quant.py:177-186); rotated reads spread banks
+      const int i = tid - 128, t = i >> 2, j = i & 3;
+      const float* r = xv + t * LDV + 32 * j;
+      lo = hi = r[j];
+      for (int k = 1; k < 32; ++k) {
+        const float x = r[(k + j) & 31];
+        lo = fminf(lo, x);
+        hi = fmaxf(hi, x);
+      }
+      B.vparams[bi * (size_t)G.rec + vpi(G, t, j)] =
+          float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+      atomicMax(reinterpret_cast<unsigned*>(&s_rv), __float_as_uint(hi - lo));
+      gidx = i;
+    }
+    const GroupParams p = params_from_minmax((double)lo, (double)hi, BITS);
+    float thr = CUDART_INF_F, rs = 0.f, zf = 0.f;
+    if (p.scale != 0.0) {
+      if (BITS == 1) {
+        thr = __double2float_ru(__dadd_rn(p.zero, __ddiv_rn(p.scale, 2.0)));
+      } else {
+        zf = (float)p.zero;  // = lo, exact
+        rs = (float)(1.0 / p.scale);
+      }
+    }
+    if (key) {
+      kz[gidx] = zf; krs[gidx] = rs; kthr[gidx] = thr; kz64[gidx] = p.zero; ks64[gidx] = p.scale;
+    } else {
+      vz[gidx] = zf; vrs[gidx] = rs; vthr[gidx] = thr; vz64[gidx] = p.zero; vs64[gidx] = p.scale;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {  // per-(seq, head) range maxima: exponent choice of the MMA path
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 2 + 0], __float_as_uint(s_rk));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 2 + 1], __float_as_uint(s_rv));
+  }
+  // Fast code of element x in its group: 1-bit x >= thr; 2-bit rint via the
+  // 1.5*2^23 magic add (round-to-nearest-even, as rint) clipped to 3.  `near`
+  // flags q within 1e-5 of a rounding boundary (or a non-finite q); such codes
+  // are redone below in float64 (quantize_code).  Degenerate groups have
+  // rs = 0 -> q = 0 -> code 0 and thr = +inf (quant.py:79-80).
+  auto fast_code = [&](float x, float z, float rs, float thr, bool& near) -> uint32_t {
+    if (BITS == 1) return x >= thr ? 1u : 0u;
+    const float dq = (x - z) * rs;
+    const float y = dq + 12582912.0f;                  // 1.5 * 2^23: rint(dq) in the low mantissa bits
+    const float r = y - 12582912.0f;                   // rint(dq), exact for 0 <= dq < 2^22
+    near |= fabsf(fabsf(dq - r) - 0.5f) < 1e-5f || !(dq < 4194304.f);
+    const uint32_t c = __float_as_uint(y) & 0x3FFFFFu;
+    return c < 3u ? c : 3u;
+  };
+  constexpr int KW = g * 4 * BITS;  // key (and value) code words per block: 256 (2-bit) / 128 (1-bit)
+  constexpr int PER = 32 / BITS;    // codes per word
+  uint32_t* okc = B.kcodes + bi * (size_t)G.rec;
+  uint32_t* ovc = B.vcodes + bi * (size_t)G.rec;
+  for (int w = tid; w < KW; w += 256) {
+    // key word: token t, channels c0 .. c0 + PER - 1, LSB first (kloc); start rotated by the run index
+    {
+      const int t = w / (4 * BITS), run = w % (4 * BITS), c0 = run * PER, rot = (2 * run) % PER;
+      uint32_t word = 0;
+      bool near = false;
+#pragma unroll
+      for (int jj = 0; jj < PER; ++jj) {
+        const int j = (jj + rot) % PER, c = c0 + j;
+        word |= fast_code(xk[t * LDK + c], kz[c], krs[c], kthr[c], near) << (BITS * j);
+      }
+      if (BITS == 2 && near) {  // rare: exact float64 codes for the whole word
+        word = 0;
+        for (int j = 0; j < PER; ++j) {
+          const int c = c0 + j;
+          word |= quantize_code(xk[t * LDK + c], GroupParams{kz64[c], ks64[c]}, 2) << (BITS * j);
+        }
+      }
+      okc[w] = word;
+    }
+    // value word: inverse of vloc (common.cuh)
+    {
+      int mt_base, lane;
+      if (BITS == 2) {
+        mt_base = 4 * (w >> 7) + (w & 3);
+        lane = (w >> 2) & 31;
+      } else {
+        mt_base = 2 * (w & 3);
+        lane = w >> 2;
+      }
+      const int gq = lane >> 2, tq = lane & 3;
+      auto tc = [&](int j, int& t, int& c) {
+        const int bit = BITS * j, odd = bit >> 4, r = (bit & 15) / BITS;
+        const int mt = BITS == 2 ? mt_base : mt_base + (r >> 3);
+        const int rh = BITS == 2 ? (r >> 2) : ((r >> 2) & 1);
+        const int q = r & 3;
+        c = 16 * mt + 8 * rh + gq;
+        t = 16 * (q >> 1) + 8 * (q & 1) + 2 * tq + odd;
+      };
+      uint32_t word = 0;
+      bool near = false;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        int t, c;
+        tc(j, t, c);
+        const int gi = t * 4 + (c >> 5);
+        word |= fast_code(xv[t * LDV + c], vz[gi], vrs[gi], vthr[gi], near) << (BITS * j);
+      }
+      if (BITS == 2 && near) {
+        word = 0;
+        for (int j = 0; j < PER; ++j) {
+          int t, c;
+          tc(j, t, c);
+          const int gi = t * 4 + (c >> 5);
+          word |= quantize_code(xv[t * LDV + c], GroupParams{vz64[gi], vs64[gi]}, 2) << (BITS * j);
+        }
+      }
+      ovc[w] = word;
+    }
+  }
+}
+
 size_t quantize_smem_bytes(const Geo& G) {
   size_t s = 2 * sizeof(float) * G.g * G.d;
   s += sizeof(uint32_t) * (2 * G.bwords + 2);
@@ -131,6 +319,11 @@ void launch_quantize(const Geo& G, const LayerBufs& B, const QuantSrc& S, int bl
     configured = true;
   }
   dim3 grid(nblocks, G.H, G.batch);
+  if (G.fast && G.d == 128 && G.g == 32 && (G.bits == 1 || G.bits == 2)) {
+    if (G.bits == 2) k_quantize_fast<2><<<grid, 256, 0, st>>>(G, B, S, blk0);
+    else k_quantize_fast<1><<<grid, 256, 0, st>>>(G, B, S, blk0);
+    return;
+  }
   k_quantize<<<grid, 256, quantize_smem_bytes(G), st>>>(G, B, S, blk0);
 }
 

@@ -145,3 +145,29 @@ def test_full_size_c2_layer_properties():
     k, v, _ = cache.slow_fetch(0, [0, 12345, n - 1], seq)
     assert np.array_equal(k, Ks[[0, 12345, n - 1]])
     cache.close()
+
+
+@pytest.mark.parametrize("bits", [1, 2])
+def test_fast_quantizer_tie_heavy_bit_exact(bits):
+    """Fast-layout K1 (d=128, g=32) on integer-grid rows: (x - z)/s lands
+    exactly on the 0.5 / 1.5 / 2.5 rounding boundaries for many elements, so
+    the float64 fallback of the fp32 code path (and rint's half-even) is
+    exercised; codes and fp16 params must equal the oracle bit for bit."""
+    from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
+    rng = np.random.default_rng(40 + bits)
+    n, H, d = 32 * 24 + 70, 2, 128
+    K = rng.integers(-3, 4, size=(n, H, d)).astype(np.float32) * 0.5      # grid of 0.5: ranges of 1..3
+    V = rng.integers(0, 7, size=(n, H, d)).astype(np.float32) * 0.25
+    K[:, :, 5] = 1.0          # a degenerate key channel (scale 0)
+    V[7, 1, 32:64] = -2.0     # a degenerate value group
+    budget = CacheBudget(bits=bits, group_size=32, residual=64, prefetch_k=16, context_length=n + 8)
+    cache = DeviceTwoTierCache(1, H, d, budget)
+    cache.prefill(0, K[None], V[None])
+    f = R.frontier(n, 64, 32)
+    e = cache.export_packed(0)
+    o = R.normative_export(K[:f], V[:f], f, bits, 32)
+    for key in ("key_codes", "val_codes"):
+        assert np.array_equal(e[key], o[key]), key
+    for key in ("key_zero", "key_scale", "val_zero", "val_scale"):
+        assert np.array_equal(e[key].view(np.uint16), o[key].view(np.uint16)), key
+    cache.close()
