@@ -225,15 +225,16 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
   }
   // Fast code of element x in its group: 1-bit x >= thr; 2-bit rint via the
   // 1.5*2^23 magic add (round-to-nearest-even, as rint) clipped to 3.  `near`
-  // flags q within 1e-5 of a rounding boundary (or a non-finite q); such codes
-  // are redone below in float64 (quantize_code).  Degenerate groups have
+  // flags q within 1e-5 of a rounding boundary (or a non-finite q); those
+  // elements alone are redone in float64 (quantize_code) after the word's
+  // fast pass -- a short divergent loop, usually one element.  Degenerate groups have
   // rs = 0 -> q = 0 -> code 0 and thr = +inf (quant.py:79-80).
   auto fast_code = [&](float x, float z, float rs, float thr, bool& near) -> uint32_t {
     if (BITS == 1) return x >= thr ? 1u : 0u;
     const float dq = (x - z) * rs;
     const float y = dq + 12582912.0f;                  // 1.5 * 2^23: rint(dq) in the low mantissa bits
     const float r = y - 12582912.0f;                   // rint(dq), exact for 0 <= dq < 2^22
-    near |= fabsf(fabsf(dq - r) - 0.5f) < 1e-5f || !(dq < 4194304.f);
+    near = fabsf(fabsf(dq - r) - 0.5f) < 1e-5f || !(dq < 4194304.f);
     const uint32_t c = __float_as_uint(y) & 0x3FFFFFu;
     return c < 3u ? c : 3u;
   };
@@ -245,19 +246,19 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
     // key word: token t, channels c0 .. c0 + PER - 1, LSB first (kloc); start rotated by the run index
     {
       const int t = w / (4 * BITS), run = w % (4 * BITS), c0 = run * PER, rot = (2 * run) % PER;
-      uint32_t word = 0;
-      bool near = false;
+      uint32_t word = 0, nmask = 0;
 #pragma unroll
       for (int jj = 0; jj < PER; ++jj) {
         const int j = (jj + rot) % PER, c = c0 + j;
+        bool near;
         word |= fast_code(xk[t * LDK + c], kz[c], krs[c], kthr[c], near) << (BITS * j);
+        if (BITS == 2) nmask |= (uint32_t)near << j;
       }
-      if (BITS == 2 && near) {  // rare: exact float64 codes for the whole word
-        word = 0;
-        for (int j = 0; j < PER; ++j) {
-          const int c = c0 + j;
-          word |= quantize_code(xk[t * LDK + c], GroupParams{kz64[c], ks64[c]}, 2) << (BITS * j);
-        }
+      while (BITS == 2 && nmask) {  // rare: exact float64 code of each boundary element
+        const int j = __ffs(nmask) - 1, c = c0 + j;
+        nmask &= nmask - 1u;
+        const uint32_t cd = quantize_code(xk[t * LDK + c], GroupParams{kz64[c], ks64[c]}, 2);
+        word = (word & ~(3u << (2 * j))) | (cd << (2 * j));
       }
       okc[w] = word;
     }
@@ -280,23 +281,24 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
         c = 16 * mt + 8 * rh + gq;
         t = 16 * (q >> 1) + 8 * (q & 1) + 2 * tq + odd;
       };
-      uint32_t word = 0;
-      bool near = false;
+      uint32_t word = 0, nmask = 0;
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         int t, c;
         tc(j, t, c);
         const int gi = t * 4 + (c >> 5);
+        bool near;
         word |= fast_code(xv[t * LDV + c], vz[gi], vrs[gi], vthr[gi], near) << (BITS * j);
+        if (BITS == 2) nmask |= (uint32_t)near << j;
       }
-      if (BITS == 2 && near) {
-        word = 0;
-        for (int j = 0; j < PER; ++j) {
-          int t, c;
-          tc(j, t, c);
-          const int gi = t * 4 + (c >> 5);
-          word |= quantize_code(xv[t * LDV + c], GroupParams{vz64[gi], vs64[gi]}, 2) << (BITS * j);
-        }
+      while (BITS == 2 && nmask) {
+        const int j = __ffs(nmask) - 1;
+        nmask &= nmask - 1u;
+        int t, c;
+        tc(j, t, c);
+        const int gi = t * 4 + (c >> 5);
+        const uint32_t cd = quantize_code(xv[t * LDV + c], GroupParams{vz64[gi], vs64[gi]}, 2);
+        word = (word & ~(3u << (2 * j))) | (cd << (2 * j));
       }
       ovc[w] = word;
     }
