@@ -109,3 +109,33 @@ def test_memory_ratio_table():
                                    (32768, 2, 32, 0.19), (32768, 1, 64, 0.10),
                                    (8192, 1, 32, 0.14), (8192, 2, 64, 0.17)]:
         assert R.memory_ratio(bits, g, length, 128) == ratio
+
+
+def test_quantizer_kats():
+    # test_quant.py:10-24 (params), 35-59 (codes, clamp, degenerate), 63-72 (levels, round trip)
+    z, s = R.quant_params(np.array([[0.0, 0.3, 1.0]]), 1)
+    assert (z[0], s[0]) == (0.25, 0.5)
+    z, s = R.quant_params(np.array([[0.0, 1.0, 2.0, 3.0]]), 2)
+    assert (z[0], s[0]) == (0.0, 1.0)
+    z, s = R.quant_params(np.array([[7.0, 7.0, 7.0]]), 2)
+    assert (z[0], s[0]) == (7.0, 0.0)
+    g = np.array([[0.0, 0.3, 0.5, 1.0]])
+    assert R.quantize(g, *R.quant_params(g, 1), 1)[0].tolist() == [0, 0, 1, 1]   # boundary maps up
+    g = np.array([[0.0, 1.0, 2.0, 3.0]])
+    zs = R.quant_params(g, 2)
+    c = R.quantize(g, *zs, 2)
+    assert c[0].tolist() == [0, 1, 2, 3]
+    assert R.dequantize(c, *zs)[0].tolist() == [0.0, 1.0, 2.0, 3.0]
+    g = np.array([[3.0, 3.0]])
+    zs = R.quant_params(g, 2)
+    assert R.quantize(g, *zs, 2)[0].tolist() == [0, 0]
+    assert R.dequantize(R.quantize(g, *zs, 2), *zs)[0].tolist() == [3.0, 3.0]
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        g = (rng.standard_normal(int(rng.integers(2, 40))) * rng.uniform(0.1, 10))[None]
+        for bits in (1, 2, 4):
+            c = R.quantize(g, *R.quant_params(g, bits), bits)
+            assert c.min() >= 0 and c.max() <= (1 << bits) - 1
+    g = np.concatenate([[0.0, 1.0], rng.random(14)])[None]
+    zs = R.quant_params(g, 1)
+    assert set(np.unique(R.dequantize(R.quantize(g, *zs, 1), *zs))) <= {np.float32(0.25), np.float32(0.75)}
