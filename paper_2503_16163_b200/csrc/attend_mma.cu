@@ -46,7 +46,10 @@
 namespace spc {
 namespace {
 
-constexpr int kWarps = 8;
+#ifndef SPC_K2_WARPS
+#define SPC_K2_WARPS 8
+#endif
+constexpr int kWarps = SPC_K2_WARPS;
 constexpr int kThreads = kWarps * 32;
 #ifndef SPC_K2_STAGES
 #define SPC_K2_STAGES 3
@@ -1393,7 +1396,7 @@ int launch_attend_fast(const AttnArgs& a0, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return 2 * sms;
+    return kMinBlocks * sms;
   }();
   static const int forced = [] {
     const char* e = getenv("SPC_NSPLIT");  // tuning only: exact split count (0 = model)
