@@ -350,8 +350,36 @@ void launch_copy_pins(const Geo& G, const LayerBufs& B, int seq, int unit, const
 
 // K6a: append row 0 at position n to the residual ring (compute stream; the
 // ring slot n % (r+g) is not read by this step's attention).
+// One thread per 16-byte chunk (8 bf16) of the (seq, head, channel) row, grid
+// (ceil(H*d/8 / 128), batch): a single wide pass instead of a 2-byte loop.
 __global__ void k_ring_append(Geo G, LayerBufs B, const __nv_bfloat16* kr, const __nv_bfloat16* vr,
                               long long seq_stride, int n) {
+  const int b = blockIdx.y, x = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (x >= G.H * G.d) return;
+  const int slot = n % G.ring, h = x / G.d, c = x - h * G.d;
+  const size_t ro = (((size_t)b * G.H + h) * G.ring + slot) * G.d + c;
+  *reinterpret_cast<uint4*>(B.ring_k + ro) = *reinterpret_cast<const uint4*>(kr + (size_t)b * seq_stride + x);
+  *reinterpret_cast<uint4*>(B.ring_v + ro) = *reinterpret_cast<const uint4*>(vr + (size_t)b * seq_stride + x);
+}
+
+// K6b: persist the row to the slow tier (pinned host, zero-copy 16-byte stores)
+// from its ring slot (copy stream).
+__global__ void k_host_append(Geo G, LayerBufs B, int n, __nv_bfloat16* host_k, __nv_bfloat16* host_v) {
+  const int b = blockIdx.y, x = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (x >= G.H * G.d) return;
+  const int slot = n % G.ring, h = x / G.d, c = x - h * G.d;
+  const size_t ro = (((size_t)b * G.H + h) * G.ring + slot) * G.d + c;
+  const size_t ho = (((size_t)b * G.L + n) * G.H + h) * G.d + c;
+  *reinterpret_cast<uint4*>(host_k + ho) = *reinterpret_cast<const uint4*>(B.ring_k + ro);
+  *reinterpret_cast<uint4*>(host_v + ho) = *reinterpret_cast<const uint4*>(B.ring_v + ro);
+}
+
+static bool rows_vectorizable(const Geo& G, long long seq_stride, const void* a, const void* b) {
+  return G.d % 8 == 0 && seq_stride % 8 == 0 && ((uintptr_t)a & 15) == 0 && ((uintptr_t)b & 15) == 0;
+}
+
+__global__ void k_ring_append_scalar(Geo G, LayerBufs B, const __nv_bfloat16* kr, const __nv_bfloat16* vr,
+                                     long long seq_stride, int n) {
   const int b = blockIdx.x;
   const int slot = n % G.ring;
   for (int x = threadIdx.x; x < G.H * G.d; x += blockDim.x) {
@@ -362,9 +390,7 @@ __global__ void k_ring_append(Geo G, LayerBufs B, const __nv_bfloat16* kr, const
   }
 }
 
-// K6b: persist the row to the slow tier (pinned host, zero-copy store) from its
-// ring slot (copy stream).
-__global__ void k_host_append(Geo G, LayerBufs B, int n, __nv_bfloat16* host_k, __nv_bfloat16* host_v) {
+__global__ void k_host_append_scalar(Geo G, LayerBufs B, int n, __nv_bfloat16* host_k, __nv_bfloat16* host_v) {
   const int b = blockIdx.x;
   const int slot = n % G.ring;
   for (int x = threadIdx.x; x < G.H * G.d; x += blockDim.x) {
@@ -378,12 +404,22 @@ __global__ void k_host_append(Geo G, LayerBufs B, int n, __nv_bfloat16* host_k, 
 
 void launch_ring_append(const Geo& G, const LayerBufs& B, const __nv_bfloat16* k_rows,
                         const __nv_bfloat16* v_rows, long long seq_stride, int n, cudaStream_t st) {
-  k_ring_append<<<G.batch, 256, 0, st>>>(G, B, k_rows, v_rows, seq_stride, n);
+  if (rows_vectorizable(G, seq_stride, k_rows, v_rows)) {
+    const int chunks = G.H * G.d / 8;
+    k_ring_append<<<dim3((chunks + 127) / 128, G.batch), 128, 0, st>>>(G, B, k_rows, v_rows, seq_stride, n);
+  } else {
+    k_ring_append_scalar<<<G.batch, 256, 0, st>>>(G, B, k_rows, v_rows, seq_stride, n);
+  }
 }
 
 void launch_host_append(const Geo& G, const LayerBufs& B, int n, __nv_bfloat16* host_k,
                         __nv_bfloat16* host_v, cudaStream_t st) {
-  k_host_append<<<G.batch, 256, 0, st>>>(G, B, n, host_k, host_v);
+  if (G.d % 8 == 0) {
+    const int chunks = G.H * G.d / 8;
+    k_host_append<<<dim3((chunks + 127) / 128, G.batch), 128, 0, st>>>(G, B, n, host_k, host_v);
+  } else {
+    k_host_append_scalar<<<G.batch, 256, 0, st>>>(G, B, n, host_k, host_v);
+  }
 }
 
 // Prefill: residual rows [f, n) of K/V [b][n][H][d] into the ring.
