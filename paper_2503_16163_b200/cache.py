@@ -38,8 +38,10 @@ def to_device_bf16(x, device):
     if isinstance(x, torch.Tensor):
         t = x.to(device=device, dtype=torch.bfloat16)
     else:
-        t = torch.from_numpy(np.ascontiguousarray(np.asarray(x, np.float32))).to(device=device,
-                                                                                   dtype=torch.bfloat16)
+        a = np.ascontiguousarray(np.asarray(x, np.float32))
+        if not a.flags.writeable:  # e.g. np.broadcast_to views: torch wants a writable buffer
+            a = a.copy()
+        t = torch.from_numpy(a).to(device=device, dtype=torch.bfloat16)
     return t.contiguous()
 
 

@@ -168,6 +168,10 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
   const Geo& G = c->G;
   if (append_row0 && c->n[layer] >= c->context_length)
     return fail(SPC_EINVAL, "context_length exceeded");
+  if (!q || !k_new || !v_new || !out) return fail(SPC_EINVAL, "null q / k_new / v_new / out");
+  // rows are read with 8- and 16-byte vector loads (and cp.async) by the attend kernels
+  if (((uintptr_t)q | (uintptr_t)k_new | (uintptr_t)v_new | (uintptr_t)out) & 15)
+    return fail(SPC_EINVAL, "q, k_new, v_new and out must be 16-byte aligned device pointers");
   AttnArgs a{};
   a.G = G;
   a.B = c->L[layer];

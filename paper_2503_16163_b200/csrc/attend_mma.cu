@@ -1413,7 +1413,7 @@ int launch_attend_fast(const AttnArgs& a0, cudaStream_t st) {
     long long best = -1;
     want = 1;
     for (int w = 1; w <= cap; ++w) {
-      const int bps = (nblk + w - 1) / w, ns = (nblk + bps - 1) / bps;
+      const int bps = std::max(1, (nblk + w - 1) / w), ns = std::max(1, (nblk + bps - 1) / bps);
       const long long rounds = ((long long)units * (ns + 1) + slots - 1) / slots;  // + the exact CTA
       const long long cost = rounds * (bps + c0);
       if (best < 0 || cost < best) {

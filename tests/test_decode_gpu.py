@@ -163,6 +163,14 @@ def test_kv_head_scope_vs_oracle():
     _oracle_run((2, 1200, 4, 16, 128, 1, 32, 64, 16, "kv_head"), seed=21)
 
 
+@pytest.mark.parametrize("n0,Hq", [(50, 4), (95, 8)])
+def test_fast_path_short_prompt(n0, Hq):
+    """d=128 fast path with an empty packed tier (f = 0: every row in the
+    residual window) and, for n0 = 95, the first migration (f: 0 -> 32) inside
+    the decode steps."""
+    _oracle_run((2, n0, 4 if Hq == 4 else 2, Hq, 128, 2, 32, 64, 16, "layer"), seed=33)
+
+
 def test_many_pins_multi_chunk_exact_segment():
     """k=200 pins + residual > 128 rows: the staged exact segment (NR <= 4)
     runs three chunks, with the pinned-only stats crossing chunk borders."""
