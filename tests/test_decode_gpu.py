@@ -221,3 +221,50 @@ def test_protocol_errors():
     with pytest.raises(ProtocolError):
         cache.prefill(0, K[None], V[None])                   # prefill may only run once
     cache.close()
+
+
+def test_long_context_fast_matches_generic():
+    """C3 geometry on one sequence (GQA-4, 1-bit, k=128) at 128k context: the
+    MMA fast path against the float64-exact generic kernel, both on the device
+    (the oracle is too slow at this length) -- outputs, pinned mass and top-k
+    sets (up to the near-tie band of the generic path's aggregate)."""
+    import torch
+    from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
+    H, Hq, d, n0, k = 8, 32, 128, 131072, 128
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    K = (torch.randn((1, n0, H, d), device="cuda", generator=gen) +
+         2 * torch.randn((1, 1, H, d), device="cuda", generator=gen))
+    V = torch.randn((1, n0, H, d), device="cuda", generator=gen)
+    q0 = torch.randn((1, 2, Hq, d), device="cuda", generator=gen) * 2
+    idx = torch.randint(0, n0 - 100, (128,), device="cuda", generator=gen)
+    for h in range(H):  # planted needles along each kv head's first q head
+        K[0, idx, h] += 0.5 * q0[0, 1, h * (Hq // H)]
+    K, V = K.to(torch.bfloat16), V.to(torch.bfloat16)
+    budget = CacheBudget(bits=1, group_size=32, residual=64, prefetch_k=k, context_length=n0 + 16)
+    caches, decs = [], []
+    for impl in ("fast", "generic"):
+        c = DeviceTwoTierCache(1, H, d, budget, q_heads=Hq, host_layers=1)
+        c.set_attend_impl(impl)
+        c.prefill(0, K, V)
+        caches.append(c)
+        decs.append(_dec(c))
+    steps = [(q0 + 0.3 * t * torch.randn(q0.shape, device="cuda", generator=gen),
+              torch.randn((1, 2, H, d), device="cuda", generator=gen),
+              torch.randn((1, 2, H, d), device="cuda", generator=gen)) for t in range(3)]
+    steps = [tuple(x.to(torch.bfloat16) for x in s) for s in steps]
+    outs = [dec.predecode_layer(0, steps[0][0][:, :1], steps[0][1][:, :1], steps[0][2][:, :1]) for dec in decs]
+    torch.cuda.synchronize()
+    o_f, o_g = outs[0].float(), outs[1].float()
+    assert (o_f - o_g).norm() / o_g.norm() <= 2e-3
+    for t in (1, 2):
+        agg_g = decs[1].debug_agg(0)[0, 0].cpu().numpy()
+        sets = [[p for p in dec.ticket(0)[0][0, 0].tolist() if p >= 0] for dec in decs]
+        assert_topk_equivalent(sets[0], sets[1], agg_g, k)
+        res = [dec.decode_layer(0, t, *steps[t]) for dec in decs]
+        torch.cuda.synchronize()
+        o_f, o_g = res[0].out.float(), res[1].out.float()
+        assert (o_f - o_g).norm() / o_g.norm() <= 2e-3, f"step {t}"
+        np.testing.assert_allclose(res[0].pinned_mass.cpu().numpy(), res[1].pinned_mass.cpu().numpy(),
+                                   rtol=1e-3, atol=1e-6)
+    for c in caches:
+        c.close()
