@@ -268,3 +268,48 @@ def test_long_context_fast_matches_generic():
                                    rtol=1e-3, atol=1e-6)
     for c in caches:
         c.close()
+
+
+@pytest.mark.parametrize("bits,H,Hq", [(2, 4, 4), (1, 2, 8)])
+def test_fully_pinned_leading_blocks(bits, H, Hq):
+    """Needles planted at positions 0..63 along the predecode query make the
+    first ticket pin two whole 32-token blocks at the start of split 0, so
+    warps 0 and 1 meet a fully masked block first (running max still -inf at
+    their first P).  Outputs, pinned mass and top-k must match the oracle."""
+    import torch
+    from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
+    rng = np.random.default_rng(77 + bits)
+    n0, d, g, r, k = 2048, 128, 32, 64, 64
+    G = Hq // H
+    K, V = make_kv(rng, n0, H, d)
+    q = make_queries(rng, 1, Hq, d)
+    for h in range(H):  # strong needles along each kv head's q heads
+        K[:64, h] = R.bf16_round(K[:64, h] + 3.0 * q[0, h * G:(h + 1) * G].mean(0))
+    st = R.LayerState(H, d, bits, g, r, k, "layer")
+    st.extend(K, V)
+    budget = CacheBudget(bits=bits, group_size=g, residual=r, prefetch_k=k, context_length=n0 + 8)
+    cache = DeviceTwoTierCache(1, H, d, budget, q_heads=Hq)
+    cache.prefill(0, K[None], V[None])
+    dec = _dec(cache)
+    kn, vn = make_step_kv(rng, 1, H, d)
+    out = dec.predecode_layer(0, q[None], kn[None], vn[None]).float().cpu().numpy()
+    o = R.predecode_layer(st, q, kn, vn)
+    assert_out_close(out[0], o["out"])
+    picked = [p for p in dec.ticket(0)[0][0, 0].tolist() if p >= 0]
+    assert set(picked) == set(range(64)) == set(o["picked"][0])
+    st.pinned[0] = tuple(picked)
+    qcur = make_queries(rng, 2, Hq, d)
+    qcur[1] = q[0]  # the speculative row keeps attending to the needles
+    for t in (1, 2):
+        kn, vn = make_step_kv(rng, 2, H, d)
+        res = dec.decode_layer(0, t, qcur[None], kn[None], vn[None])
+        torch.cuda.synchronize()
+        got = res.out[0].float().cpu().numpy()
+        assert np.isfinite(got).all()
+        o = R.decode_layer(st, qcur, kn, vn)
+        assert_out_close(got, o["out"])
+        np.testing.assert_allclose(res.pinned_mass[0].cpu().numpy(), o["pinned_mass"], rtol=1e-4, atol=1e-6)
+        picked = [p for p in dec.ticket(0)[0][0, 0].tolist() if p >= 0]
+        assert_topk_equivalent(picked, list(o["picked"][0]), o["agg"][0], k)
+        st.pinned[0] = tuple(sorted(picked))
+    cache.close()
