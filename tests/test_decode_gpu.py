@@ -39,6 +39,21 @@ def assert_out_close(got, exp):
     assert np.abs(got - exp).max() <= 4e-3 * np.abs(exp).max()
 
 
+def assert_out_close_rows(got, exp):
+    """As assert_out_close, with the 2e-3 bound on each row's full attention
+    output (all heads) and 3e-3 per head (see test_long_run_ring_wrap_and_migrations)."""
+    got = np.asarray(got, np.float32).reshape(exp.shape[0], -1, exp.shape[-1])
+    exp = exp.reshape(got.shape)
+    exp16 = R.bf16_round(exp)
+    for r in range(exp.shape[0]):
+        e = np.linalg.norm(got[r] - exp16[r]) / max(np.linalg.norm(exp[r]), 1e-30)
+        assert e <= OUT_RTOL, f"row {r}: rel err {e:.2e}"
+        for h in range(exp.shape[1]):
+            e = np.linalg.norm(got[r, h] - exp16[r, h]) / max(np.linalg.norm(exp[r, h]), 1e-30)
+            assert e <= 1.5 * OUT_RTOL, f"row {r} head {h}: rel err {e:.2e}"
+    assert np.abs(got - exp).max() <= 4e-3 * np.abs(exp).max()
+
+
 def assert_topk_equivalent(got, exp, agg_ref, k):
     got, exp = set(got), set(exp)
     if got == exp:
@@ -93,7 +108,7 @@ def test_decode_layer_matches_reference_run(tag, impl):
     cache.close()
 
 
-def _oracle_run(cfg, seed, steps=3, impl="auto"):
+def _oracle_run(cfg, seed, steps=3, impl="auto", per_row=False):
     """Seeded C1-like run: device vs oracle for predecode + `steps` decode steps."""
     import torch
     from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
@@ -135,7 +150,10 @@ def _oracle_run(cfg, seed, steps=3, impl="auto"):
         picked, newc = dec.ticket(0)
         for s in range(b):
             o = R.decode_layer(states[s], qcur[s], kn[s], vn[s])
-            assert_out_close(outs[s], o["out"])
+            if per_row:
+                assert_out_close_rows(outs[s], o["out"])
+            else:
+                assert_out_close(outs[s], o["out"])
             np.testing.assert_allclose(pm[s], o["pinned_mass"], rtol=1e-4, atol=1e-6)
             for u in range(U):
                 got = [p for p in picked[s, u].tolist() if p >= 0]
@@ -313,3 +331,20 @@ def test_fully_pinned_leading_blocks(bits, H, Hq):
         assert_topk_equivalent(picked, list(o["picked"][0]), o["agg"][0], k)
         st.pinned[0] = tuple(sorted(picked))
     cache.close()
+
+
+@pytest.mark.parametrize("H,Hq,bits", [(2, 2, 2), (2, 8, 1)])
+def test_long_run_ring_wrap_and_migrations(H, Hq, bits):
+    """70 decode steps on the fast path with r = g = 32 (ring of 64 slots): the
+    residual ring wraps and the frontier migrates twice mid-run.
+
+    Every step must match the oracle: identical top-k sets (up to the near-tie
+    band), pinned mass, and outputs within 2e-3 of the bf16-rounded reference
+    for each row as a whole (all heads).  Per head the bound is 3e-3.  Over
+    70 x 16 x 2 head-rows, the per-head comparison of two bf16-rounded results
+    sees occasional 1-ulp flips.  The kernel's score arithmetic errs by about
+    1.5e-6 (the zero-point sum) plus 1e-6 (the hi/lo operand split).  The
+    reference's own fp32 scores err by 1.7e-6 against exact arithmetic
+    (tools/precision_probe.py), so these flips are rounding noise
+    on both sides, not a kernel error."""
+    _oracle_run((1, 700, H, Hq, 128, bits, 32, 32, 16, "layer"), seed=41 + bits, steps=70, per_row=True)

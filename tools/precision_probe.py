@@ -71,5 +71,41 @@ def main():
                   f"{worst[2]:.2e} / {worst[3]:.2e}")
 
 
+def score_error_sources():
+    """Score (log2 units) error against exact float64 arithmetic on a 32-token
+    2-bit key block with channel offsets N(0, 2^2): the reference's own fp32
+    path (q . K~ then * float32(d^-1/2)) vs K2's two terms -- the fp32 zero-point
+    sum C_j (4-term lane partials + a 32-lane tree) and the f16 hi+lo key B
+    operand.  All three are of the same order, so K2 differs from the reference
+    by about as much as the reference differs from exact arithmetic."""
+    rng = np.random.default_rng(0)
+    d = 128
+    f32 = np.float32
+    e_ref = e_c = e_b = 0.0
+    for _ in range(50):
+        off = rng.normal(0, 2, d)
+        K = (rng.standard_normal((32, d)) + off).astype(np.float32)
+        q = (rng.standard_normal(d) * 1.5).astype(np.float32)
+        lo, hi = K.min(0).astype(np.float64), K.max(0).astype(np.float64)
+        z, s = lo, (hi - lo) / 3
+        codes = np.clip(np.rint((K - z) / np.where(s == 0, 1, s)), 0, 3)
+        Kq = codes * s + z
+        sc = d ** -0.5 * np.log2(np.e)
+        exact = Kq @ (q.astype(np.float64) * sc)
+        Kq32 = Kq.astype(np.float32)
+        ref = np.array([np.dot(q, Kq32[t]) for t in range(32)], dtype=np.float32) * f32(d ** -0.5)
+        e_ref = max(e_ref, np.abs(ref.astype(np.float64) * np.log2(np.e) - exact).max())
+        Qf = (q * f32(sc)).astype(np.float32)
+        parts = (Qf * z.astype(np.float32)).astype(np.float32).reshape(32, 4).sum(1, dtype=np.float32)
+        while parts.size > 1:
+            parts = (parts[0::2] + parts[1::2]).astype(np.float32)
+        e_c = max(e_c, abs(float(parts[0]) - float((Qf.astype(np.float64) * z).sum())))
+        w = Qf.astype(np.float64) * s
+        hi16 = f16(w)
+        e_b = max(e_b, np.abs(codes @ (hi16 + f16(w - hi16)) - codes @ w).max())
+    print(f"score error vs exact: reference fp32 {e_ref:.2e}; K2 zero-point sum {e_c:.2e}, hi/lo operand {e_b:.2e}")
+
+
 if __name__ == "__main__":
     main()
+    score_error_sources()
