@@ -50,6 +50,11 @@ CONFIGS = {
                         "over 8 GPUs (4 per rank), 1-bit KV (g32, r64), top-k 256, full bf16 cache in pinned host",
                layers=32, batch=4, kv_heads=8, q_heads=32, head_dim=128, ctx=131072, bits=1,
                group=32, residual=64, topk=256),
+    # C3's geometry at 2 bits (not a BASELINE config): the 2-bit x 8-row K2 instantiation
+    "c3b2": dict(workload="C3 geometry at 2-bit: Mistral-7B-shaped GQA (8 KV heads) 32-layer decode, ctx 128k, "
+                          "batch 8, 2-bit KV (g32, r64), top-k 128",
+                 layers=32, batch=8, kv_heads=8, q_heads=32, head_dim=128, ctx=131072, bits=2,
+                 group=32, residual=64, topk=128),
     # BASELINE.json configs[0] (parity config; launch-bound)
     "c1": dict(workload="C1: single-layer SpeCache decode, 32 heads x d128, ctx 4096, 2-bit KV, "
                         "top-k 64, residual 32, batch 1",

@@ -58,6 +58,10 @@ constexpr int kThreads = kWarps * 32;
 #define SPC_K2_MINB 2
 #endif
 constexpr int kStages = SPC_K2_STAGES;  // TMA ring depth per warp
+// 2-bit x 8 rows (GQA-4 dual-token at 2 bits) would need 130 KB per CTA with the
+// 3-stage ring -- one CTA per SM; two stages bring it to 105 KB and two CTAs
+template <int BITS, int NR>
+constexpr int stages_of() { return (BITS == 2 && NR == 8) ? 2 : kStages; }
 constexpr int kMinBlocks = SPC_K2_MINB; // resident CTAs per SM
 #ifndef SPC_K2_LAZY
 #define SPC_K2_LAZY 1
@@ -181,7 +185,8 @@ struct __align__(16) WarpSmem {
   // row stride = 4 mod 8 uint4 so a 128-bit store phase (ks = 0..7) hits 8 distinct bank slots
   static constexpr int kBkRow = 4 * NR + ((NR & 1) ? 0 : 4);
   uint4 bk[8][kBkRow];
-  uint32_t stage[kStages][StageLayout<BITS>::words];      // TMA ring
+  static constexpr int kS = stages_of<BITS, NR>();
+  uint32_t stage[kS][StageLayout<BITS>::words];            // TMA ring
   // block probabilities: PG (<= 2 rows) [row][40]; otherwise [row & 1][token][row >> 1]
   // in 132-float planes, conflict-free for both the score-side stores (t = c+gq,
   // row = 2tq+e) and the value-side loads (row = gq, t = c+2tq)
@@ -192,7 +197,7 @@ struct __align__(16) WarpSmem {
     return NR * 4 <= 8 ? row * 40 + t : (row & 1) * 132 + t * 4 + (row >> 1);
   }
   float4 sz[64];                                          // value (s*2^-q, z) pairs, vparams order
-  uint64_t bar[kStages];
+  uint64_t bar[kS];
 };
 
 template <int NR>
@@ -692,6 +697,7 @@ __device__ void exact_segment_rows(const AttnArgs& a, const int split, const int
 
 template <int BITS, int NR>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a) {
+  constexpr int kSt = stages_of<BITS, NR>();
   // PACK: score MMA columns n = 2*row + plane (hi/lo of each row side by side),
   //       one MMA per k-step and one score row per lane (row = lane & 3).
   // PG:   P.V columns n = group*NR + row, one B fragment for all value groups.
@@ -732,10 +738,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   }
   if (lane == 0) {
 #pragma unroll
-    for (int s = 0; s < kStages; ++s) mbar_init(&ws.bar[s], 1);
+    for (int s = 0; s < kSt; ++s) mbar_init(&ws.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 #pragma unroll
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kSt; ++s) {
       const int blk = blk0 + warp + s * kWarps;
       if (blk < blk1) issue(blk, s);
     }
@@ -1090,9 +1096,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
     }
     __syncwarp();
     // the stage is consumed (codes in registers, params decoded to ws.sz): refill it
-    // with block it + kStages (async proxy after generic reads)
+    // with block it + kSt (async proxy after generic reads)
     if (lane == 0) {
-      const int nblk = blk + kStages * kWarps;
+      const int nblk = blk + kSt * kWarps;
       if (nblk < blk1) {
         fence_proxy_async();
         issue(nblk, st);
@@ -1219,9 +1225,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
       }
     }
     __syncwarp();
-    // the stage is consumed: refill it with block it + kStages (async proxy after generic reads)
+    // the stage is consumed: refill it with block it + kSt (async proxy after generic reads)
     if (lane == 0) {
-      const int nblk = blk + kStages * kWarps;
+      const int nblk = blk + kSt * kWarps;
       if (nblk < blk1) {
         fence_proxy_async();
         issue(nblk, st);
@@ -1259,7 +1265,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
     }
     }
     bm = nbm;
-    if (++st == kStages) {
+    if (++st == kSt) {
       st = 0;
       phase ^= 1u;
     }
@@ -1269,7 +1275,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   __syncwarp();
   if (lane == 0) {
 #pragma unroll
-    for (int s = 0; s < kStages; ++s)
+    for (int s = 0; s < kSt; ++s)
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&ws.bar[s])) : "memory");
   }
 #pragma unroll
@@ -1357,7 +1363,7 @@ template <int BITS, int NR>
 void launch_fast_t(const AttnArgs& a, cudaStream_t st) {
   constexpr size_t smem = fast_smem_bytes<BITS, NR>();
   // two CTAs per SM (228 KB, 1 KB reserved per CTA) is the design point
-  static_assert((BITS == 2 && NR == 8) || smem * kMinBlocks <= 227 * 1024, "K2 shared memory exceeds kMinBlocks CTAs/SM");
+  static_assert(smem * kMinBlocks <= 227 * 1024, "K2 shared memory exceeds kMinBlocks CTAs/SM");
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_attend_fast<BITS, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
