@@ -348,3 +348,46 @@ def test_long_run_ring_wrap_and_migrations(H, Hq, bits):
     (tools/precision_probe.py), so these flips are rounding noise
     on both sides, not a kernel error."""
     _oracle_run((1, 700, H, Hq, 128, bits, 32, 32, 16, "layer"), seed=41 + bits, steps=70, per_row=True)
+
+
+@pytest.mark.parametrize("k,bits", [(50, 2), (1, 1)])
+def test_odd_topk_and_degenerate_groups(k, bits):
+    """GQA-4 (8 rows) with a top-k budget that is not a multiple of 32 (or 1),
+    a constant key channel (scale 0 in every key group of that channel) and
+    constant value groups in a band of tokens: outputs, pinned mass and top-k
+    against the oracle over 5 steps."""
+    import torch
+    from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
+    rng = np.random.default_rng(90 + k)
+    n0, H, Hq, d, g, r = 900, 2, 8, 128, 32, 64
+    K, V = make_kv(rng, n0, H, d)
+    K[:, :, 5] = 1.25                 # degenerate key channel
+    V[100:164, 1, 32:64] = -0.5       # degenerate value groups (two blocks of tokens)
+    st = R.LayerState(H, d, bits, g, r, k, "layer")
+    st.extend(K, V)
+    budget = CacheBudget(bits=bits, group_size=g, residual=r, prefetch_k=k, context_length=n0 + 16)
+    cache = DeviceTwoTierCache(1, H, d, budget, q_heads=Hq)
+    cache.prefill(0, K[None], V[None])
+    dec = _dec(cache)
+    q = make_queries(rng, 1, Hq, d)
+    kn, vn = make_step_kv(rng, 1, H, d)
+    out = dec.predecode_layer(0, q[None], kn[None], vn[None]).float().cpu().numpy()
+    o = R.predecode_layer(st, q, kn, vn)
+    assert_out_close(out[0], o["out"])
+    picked = [p for p in dec.ticket(0)[0][0, 0].tolist() if p >= 0]
+    assert_topk_equivalent(picked, list(o["picked"][0]), o["agg"][0], k)
+    st.pinned[0] = tuple(sorted(picked))
+    qcur = make_queries(rng, 2, Hq, d)
+    for t in range(1, 6):
+        kn, vn = make_step_kv(rng, 2, H, d)
+        res = dec.decode_layer(0, t, qcur[None], kn[None], vn[None])
+        torch.cuda.synchronize()
+        o = R.decode_layer(st, qcur, kn, vn)
+        assert_out_close(res.out[0].float().cpu().numpy(), o["out"])
+        np.testing.assert_allclose(res.pinned_mass[0].cpu().numpy(), o["pinned_mass"], rtol=1e-4, atol=1e-6)
+        picked = [p for p in dec.ticket(0)[0][0, 0].tolist() if p >= 0]
+        assert len(picked) == min(k, cache.quantized_frontier(0))
+        assert_topk_equivalent(picked, list(o["picked"][0]), o["agg"][0], k)
+        st.pinned[0] = tuple(sorted(picked))
+        qcur = R.bf16_round((qcur + 0.3 * rng.standard_normal(qcur.shape)).astype(np.float32))
+    cache.close()
