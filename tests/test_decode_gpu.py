@@ -391,3 +391,45 @@ def test_odd_topk_and_degenerate_groups(k, bits):
         st.pinned[0] = tuple(sorted(picked))
         qcur = R.bf16_round((qcur + 0.3 * rng.standard_normal(qcur.shape)).astype(np.float32))
     cache.close()
+
+
+@pytest.mark.parametrize("kscale,vscale,tau", [(0.01, 1000.0, 1.0), (8.0, 1e-3, 1.0), (1.0, 1.0, 30.0)])
+def test_extreme_magnitudes(kscale, vscale, tau):
+    """Operand-exponent paths of the fast kernel: keys scaled by 0.01 or 8,
+    values by 1000 or 1e-3, and very peaky attention (query scale 30, the
+    lazy-rescale path raising its max often) -- MHA 2-bit against the oracle."""
+    import torch
+    from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
+    rng = np.random.default_rng(123)
+    n0, H, Hq, d, g, r, k, bits = 1200, 4, 4, 128, 32, 64, 32, 2
+    K, V = make_kv(rng, n0, H, d)
+    K, V = R.bf16_round(K * kscale), R.bf16_round(V * vscale)
+    st = R.LayerState(H, d, bits, g, r, k, "layer")
+    st.extend(K, V)
+    budget = CacheBudget(bits=bits, group_size=g, residual=r, prefetch_k=k, context_length=n0 + 16)
+    cache = DeviceTwoTierCache(1, H, d, budget, q_heads=Hq)
+    cache.prefill(0, K[None], V[None])
+    dec = _dec(cache)
+    q = make_queries(rng, 1, Hq, d, tau=tau)
+    kn, vn = make_step_kv(rng, 1, H, d)
+    kn, vn = R.bf16_round(kn * kscale), R.bf16_round(vn * vscale)
+    out = dec.predecode_layer(0, q[None], kn[None], vn[None]).float().cpu().numpy()
+    o = R.predecode_layer(st, q, kn, vn)
+    assert np.isfinite(out).all()
+    assert_out_close(out[0], o["out"])
+    picked = [p for p in dec.ticket(0)[0][0, 0].tolist() if p >= 0]
+    st.pinned[0] = tuple(sorted(picked))
+    qcur = make_queries(rng, 2, Hq, d, tau=tau)
+    for t in range(1, 4):
+        kn, vn = make_step_kv(rng, 2, H, d)
+        kn, vn = R.bf16_round(kn * kscale), R.bf16_round(vn * vscale)
+        res = dec.decode_layer(0, t, qcur[None], kn[None], vn[None])
+        torch.cuda.synchronize()
+        got = res.out[0].float().cpu().numpy()
+        assert np.isfinite(got).all()
+        o = R.decode_layer(st, qcur, kn, vn)
+        assert_out_close(got, o["out"])
+        picked = [p for p in dec.ticket(0)[0][0, 0].tolist() if p >= 0]
+        assert_topk_equivalent(picked, list(o["picked"][0]), o["agg"][0], k)
+        st.pinned[0] = tuple(sorted(picked))
+    cache.close()
