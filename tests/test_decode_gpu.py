@@ -181,6 +181,11 @@ def test_kv_head_scope_vs_oracle():
     _oracle_run((2, 1200, 4, 16, 128, 1, 32, 64, 16, "kv_head"), seed=21)
 
 
+def test_kv_head_scope_mha_2bit_vs_oracle():
+    """Per-kv-head top-k units on the MHA 2-bit (PACK/PG) instantiation."""
+    _oracle_run((2, 1300, 4, 4, 128, 2, 32, 64, 24, "kv_head"), seed=22)
+
+
 @pytest.mark.parametrize("n0,Hq", [(50, 4), (95, 8)])
 def test_fast_path_short_prompt(n0, Hq):
     """d=128 fast path with an empty packed tier (f = 0: every row in the
