@@ -52,7 +52,10 @@ class DeviceTwoTierCache:
     extra keywords are the B200 batching/placement knobs:
     batch (lockstep sequences), q_heads (GQA width, default kv_heads),
     device, topk_scope ("layer" = reference, "kv_head" = per-KV-head sets),
-    host_layers (distinct pinned-host slabs; see include/specache.h).
+    host_layers (distinct pinned-host slabs, default 0 = one per layer; a
+    smaller value aliases layer l onto slab l % host_layers, which is only
+    correct when the aliased layers are fed identical KV -- a benchmarking knob
+    for host-memory budgets, see include/specache.h).
     """
 
     def __init__(self, layers: int, kv_heads: int, head_dim: int, budget: CacheBudget, *,
