@@ -830,6 +830,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   for (int blk = blk0 + warp; blk < blk1; blk += kWarps) {
     const uint32_t nbm = (blk + kWarps < blk1) ? bm_base[blk + kWarps] : 0u;
     mbar_wait(&ws.bar[st], phase);
+    // order the previous block's reads of ws.sz / ws.P before this block's writes
+    // by other lanes (independent thread scheduling; compute-sanitizer racecheck)
+    __syncwarp();
     const uint32_t* S = ws.stage[st];
 
     // ---- key B fragments (cooperative) + zero-point constants C_j -----------------------
