@@ -1,3 +1,10 @@
+#!/usr/bin/env python
+"""cuBLAS bf16 GEMM bandwidth at decode shapes (M = 2 x batch rows): the
+full-decoder step's weight GEMMs (x @ W^T with W [N, K]), timed alone over
+four weight copies so L2 does not hold them.  Prints us and weight GB/s.
+
+  python tools/gemm_probe.py
+"""
 import torch, time
 torch.backends.cuda.matmul.allow_tf32 = False
 dev='cuda'

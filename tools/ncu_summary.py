@@ -1,3 +1,10 @@
+#!/usr/bin/env python
+"""Summarise an ncu --set full report of one kernel: time, DRAM bytes,
+occupancy limits, issue activity, tensor-pipe activity, the top warp-stall
+reasons and the opcode mix (share of instructions / of stall samples).
+
+  python tools/ncu_summary.py report.ncu-rep > profiles/<name>.txt
+"""
 import csv,sys,subprocess,collections
 rep=sys.argv[1]
 raw=subprocess.run(['ncu','-i',rep,'--page','raw','--csv'],capture_output=True,text=True).stdout
