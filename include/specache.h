@@ -116,6 +116,8 @@ SPC_API int spc_pin(spc_cache* cache, int layer, int seq, int unit, const int32_
             int npos, const void* k_rows, const void* v_rows, void* stream);
 
 /* -- the hot path ------------------------------------------------------------ */
+/* q, k_new, v_new and out of both calls must be 16-byte aligned device
+ * pointers (vector loads / cp.async); SPC_EINVAL otherwise. */
 /* Pre-decoding (engine.py:245-268): q device bf16 [batch][1][q_heads][d],
  * k_new/v_new [batch][1][kv_heads][d].  out: device bf16 [batch][1][q_heads][d].
  * Issues ticket (step 0, layer) -- top-k + prefetch on the cache's copy stream. */
