@@ -18,7 +18,10 @@ top-k 64, one B200.  Inputs are synthetic (seeded, bf16), post-RoPE q/k/v
 
 Multi-GPU (torchrun, one rank per GPU): the path shards by sequence with no
 data-path collective -- every rank runs its own batch (weak scaling); NCCL is
-used only for the barrier and the max-over-ranks timing.
+used only for the barrier and the max-over-ranks timing.  `--shard heads`
+instead splits the config's KV heads over the ranks (strong scaling, the
+north star's partitioning): each layer's partial top-k aggregate is summed
+across ranks by an NCCL all-reduce on the cache's copy stream (shard.py).
 """
 from __future__ import annotations
 
@@ -347,6 +350,33 @@ def prefill_cache(cache, cfg, host_layers, s0, device, seed):
         torch.cuda.synchronize(device)
 
 
+def agg_reducer(cache, layers, device):
+    """Per-layer cross-rank sum of the partial top-k aggregate for a KV-head
+    sharded cache (shard.py): NCCL all-reduce on the layer's copy stream, then
+    the rest of the ticket (spc_finish_layer).  Views and streams are built once."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_16163_b200 import _lib
+    from paper_2503_16163_b200.decode import _device_f32
+    lib, h = _lib.lib(), cache.handle
+    views = []
+    for layer in range(layers):
+        ptr, count, st = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_void_p()
+        _lib.check(lib.spc_agg_buffer(h, layer, ctypes.byref(ptr), ctypes.byref(count), ctypes.byref(st)))
+        views.append((_device_f32(ptr.value, count.value, device), torch.cuda.ExternalStream(st.value, device=device)))
+
+    def reduce(layer):
+        v, s = views[layer]
+        with torch.cuda.stream(s):
+            dist.all_reduce(v)
+        _lib.check(lib.spc_finish_layer(h, layer))
+
+    return reduce
+
+
 def run_gpu_arm(args, cfg):
     import numpy as np
     import torch
@@ -358,8 +388,15 @@ def run_gpu_arm(args, cfg):
     rank, world, local, local_world = dist_env()
     torch.cuda.set_device(local)
     device = f"cuda:{local}"
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(device))
+    heads = args.shard == "heads"
+    if world > 1 or heads:  # head sharding reduces the aggregate even at N=1 (a 1-rank NCCL group)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+        dist.init_process_group("nccl", device_id=torch.device(device), rank=rank, world_size=world)
+    if heads:
+        from paper_2503_16163_b200.shard import head_shard
+        sh = head_shard(cfg["kv_heads"], cfg["q_heads"], rank, world)
+        cfg = dict(cfg, kv_heads=sh.kv_heads, q_heads=sh.q_heads)
 
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -375,7 +412,13 @@ def run_gpu_arm(args, cfg):
     cache = DeviceTwoTierCache(cfg["layers"], cfg["kv_heads"], cfg["head_dim"], budget,
                                batch=cfg["batch"], q_heads=cfg["q_heads"], device=local,
                                host_layers=host_layers)
-    dec = SpeculativeLayerDecoder(cache)
+    reduce_layer = None
+    if heads:
+        from paper_2503_16163_b200.shard import allreduce_sum
+        dec = SpeculativeLayerDecoder(cache, agg_reduce=allreduce_sum())
+        reduce_layer = agg_reducer(cache, cfg["layers"], device)
+    else:
+        dec = SpeculativeLayerDecoder(cache)
     q, k_new, v_new, s0 = make_inputs(cfg, total_steps + 1, device, host_layers, seed=1234 + rank)
     prefill_cache(cache, cfg, host_layers, s0, device, seed=99 + rank)
     L = cfg["layers"]
@@ -390,6 +433,8 @@ def run_gpu_arm(args, cfg):
             _lib.check(lib.spc_decode_layer(h, layer, t, qt[layer].data_ptr(), kt[layer].data_ptr(),
                                             vt[layer].data_ptr(), out[layer].data_ptr(),
                                             pm[layer].data_ptr(), stream))
+            if reduce_layer:
+                reduce_layer(layer)
 
     # predecode (Alg. 2): first tickets
     for layer in range(L):
@@ -474,6 +519,8 @@ def run_gpu_arm(args, cfg):
                 _lib.check(lib.spc_decode_layer(h, layer, tt, q_d[layer].data_ptr(), k_d[layer].data_ptr(),
                                                 v_d[layer].data_ptr(), out[layer].data_ptr(),
                                                 pm[layer].data_ptr(), stream))
+                if reduce_layer:
+                    reduce_layer(layer)
             ev = torch.cuda.Event()
             ev.record(comp)
             cs_out.wait_event(ev)
@@ -499,7 +546,7 @@ def run_gpu_arm(args, cfg):
     d2h = o_h.numel() * 2 + pm_h.numel() * 4
 
     ms_per_step = elapsed_ms / K
-    tokens = whole_job_tokens(cfg["batch"], K, world)
+    tokens = cfg["batch"] * K if heads else whole_job_tokens(cfg["batch"], K, world)
     value = tokens / (elapsed_ms / 1e3)
     ab = algorithmic_bytes_per_layer(cfg, n_mid + K // 2, f_mid, npin)
     attn_avg_ms = attn_ms / max(1, attn_n)
@@ -522,11 +569,15 @@ def run_gpu_arm(args, cfg):
     h2d_pf = pf_bytes / K  # measured: new pins x row bytes, summed over the timed steps
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
-        "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if heads else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; peaky: %d needle keys per "
         "(seq, kv head), q drift sigma %.1f)" % (NEEDLES, DRIFT),
-        "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * world, "seq_len": cfg["ctx"],
-                   "layers": cfg["layers"], "parallelism": f"replicas-by-sequence x{world} (no collective)",
+        "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * (1 if heads else world),
+                   "seq_len": cfg["ctx"], "layers": cfg["layers"],
+                   "parallelism": (f"kv-heads x{world} ({cfg['kv_heads']} kv / {cfg['q_heads']} q heads per rank; "
+                                   "per-layer NCCL all-reduce of the top-k aggregate on the copy stream)") if heads
+                   else f"replicas-by-sequence x{world} (no collective)",
                    "bits": cfg["bits"], "topk": cfg["topk"], "l2": "no flush: per-step KV traffic "
                    "%.1f GB >> 126 MB L2" % (ab["hbm"] * cfg["layers"] / 1e9),
                    "host_layers": host_layers, "attention_impl": "fast" if cache.fast_path else "generic"},
@@ -556,7 +607,7 @@ def run_gpu_arm(args, cfg):
     if rank == 0:
         print(json.dumps(line), flush=True)
     cache.close()
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 
@@ -681,6 +732,9 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--host-layers", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="seq", choices=["seq", "heads"],
+                    help="multi-GPU partition: by sequence (no collective; default) or by KV head "
+                         "(layer-scope top-k: per-layer NCCL all-reduce of the aggregate on the copy stream)")
     ap.add_argument("--full-decoder", action="store_true",
                     help="time the whole model step around the hot path (SURVEY 8(f) row 1)")
     args = ap.parse_args()

@@ -140,6 +140,25 @@ SPC_API int spc_select_topk(const float* scores, int n, int k, int32_t* out, voi
 /* Debug: speculative-row aggregate of `layer`, device fp32 [batch][units][context_length]. */
 SPC_API int spc_debug_agg(spc_cache* cache, int layer, float* agg, void* stream);
 
+/* -- KV-head sharding with layer-scope top-k (collective (2)) -----
+ * A rank that owns kv heads [h0, h1) of every sequence builds its cache with
+ * kv_heads = h1 - h0 (q_heads likewise).  engine.py:317 sums the speculative
+ * row's probabilities over ALL q heads of the layer, so the ranks' partial
+ * aggregates must be summed before the top-k.  With spc_set_agg_reduce(c, 1),
+ * spc_decode_layer / spc_predecode_layer stop after the partial aggregate; the
+ * caller sums spc_agg_buffer's fp32 [batch][1][L] across ranks in place (e.g.
+ * an NCCL all-reduce) on the returned copy stream, then spc_finish_layer
+ * enqueues the rest of the ticket there (top-k + pin diff, PCIe prefetch,
+ * slow-tier append).  Every rank then selects the same positions.  Until
+ * spc_finish_layer, the next decode/predecode, spc_ticket, spc_debug_agg and
+ * spc_pin of that layer return SPC_EPROTO.  kv_head scope needs no exchange
+ * and no reduction. */
+SPC_API int spc_set_agg_reduce(spc_cache* cache, int enable);
+/* agg: device fp32 [batch][units][L] of `layer` (count elements); stream: the
+ * cudaStream_t the reduction must be enqueued on. */
+SPC_API int spc_agg_buffer(spc_cache* cache, int layer, float** agg, int64_t* count, void** stream);
+SPC_API int spc_finish_layer(spc_cache* cache, int layer);
+
 /* -- reads / parity ------------------------------------------------------------ */
 /* materialize (kvcache.py:222-243) for one (seq, head): device fp32 [n][d] x2,
  * bit-identical to the reference's float32 dequantization. */

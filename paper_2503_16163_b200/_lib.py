@@ -49,6 +49,9 @@ _SIGS = {
     "spc_decode_layer": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P]),
     "spc_ticket": (_I, [_P, _I, _P, _P, _P]),
     "spc_debug_agg": (_I, [_P, _I, _P, _P]),
+    "spc_set_agg_reduce": (_I, [_P, _I]),
+    "spc_agg_buffer": (_I, [_P, _I, ctypes.POINTER(_P), ctypes.POINTER(_I64), ctypes.POINTER(_P)]),
+    "spc_finish_layer": (_I, [_P, _I]),
     "spc_select_topk": (_I, [_P, _I, _I, _P, _P]),
     "spc_materialize": (_I, [_P, _I, _I, _I, _P, _P, _P]),
     "spc_export_packed": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P]),

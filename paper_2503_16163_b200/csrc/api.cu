@@ -84,6 +84,15 @@ struct spc_cache {
   int64_t launches = 0;
   double last_wait_ms = 0, last_pf_ms = 0;
   int64_t last_pf_rows = 0;
+  // head-sharded layer scope (spc_set_agg_reduce): the ticket tail waits for the
+  // caller's cross-rank reduction of agg, enqueued on the copy stream
+  bool agg_ext = false;
+  struct Pending {
+    bool on = false, append = false;
+    int f = 0, n_before = 0;
+    cudaEvent_t p0 = nullptr;
+  };
+  std::vector<Pending> pend;
 };
 
 namespace {
@@ -104,6 +113,13 @@ __nv_bfloat16* host_slab(spc_cache* c, __nv_bfloat16* base, int layer) {
 int check_layer(const spc_cache* c, int layer) {
   if (!c) return fail(SPC_EINVAL, "null cache");
   if (layer < 0 || layer >= c->G.layers) return fail(SPC_EINVAL, "layer out of range");
+  return SPC_OK;
+}
+
+int check_not_pending(const spc_cache* c, int layer) {
+  if (c->pend[layer].on)
+    return fail(SPC_EPROTO, "layer " + std::to_string(layer) +
+                                ": the aggregate awaits its cross-rank reduction (call spc_finish_layer)");
   return SPC_OK;
 }
 
@@ -161,6 +177,8 @@ cudaEvent_t prof_event(spc_cache* c) {
   }
   return c->ev_pool[c->ev_used++];
 }
+
+int ticket_tail(spc_cache* c, int layer, int f, int n_before, bool append_row0, cudaEvent_t p0);
 
 // One decode / predecode layer.  append_row0: decode persists row 0 (engine.py:321).
 int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_new,
@@ -225,12 +243,26 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
   CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_agg[layer], 0));
   if (c->prof) {
     p0 = prof_event(c);
-    p1 = prof_event(c);
     CUDA_TRY(cudaEventRecord(p0, cs));
   }
   launch_agg(a, cs);
   c->launches += a.f > 0;
-  launch_topk(G, c->L[layer], a.f, cs);
+  CUDA_TRY(cudaGetLastError());
+  if (c->agg_ext) {  // the caller reduces agg across ranks on cs, then spc_finish_layer
+    c->pend[layer] = spc_cache::Pending{true, append_row0, a.f, n_before, p0};
+    return SPC_OK;
+  }
+  return ticket_tail(c, layer, a.f, n_before, append_row0, p0);
+}
+
+// K4 top-k + pin diff -> K5 prefetch -> K6b slow-tier write (+K1 migration) on
+// the layer's copy stream, then ev_pf(layer): the rest of the ticket.
+int ticket_tail(spc_cache* c, int layer, int f, int n_before, bool append_row0, cudaEvent_t p0) {
+  const Geo& G = c->G;
+  cudaStream_t cs = c->cstream(layer);
+  cudaEvent_t p1 = nullptr;
+  if (c->prof) p1 = prof_event(c);
+  launch_topk(G, c->L[layer], f, cs);
   cudaEvent_t q0 = nullptr, q1 = nullptr;
   if (c->prof) {
     q0 = prof_event(c);
@@ -404,6 +436,7 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
   c->n.assign(G.layers, 0);
   c->f.assign(G.layers, 0);
   c->ticket.assign(G.layers, -1);
+  c->pend.assign(G.layers, spc_cache::Pending{});
   if (rc != SPC_OK) {
     std::string keep = g_err;
     spc_cache_destroy(c);
@@ -506,6 +539,7 @@ int spc_select_topk(const float* scores, int n, int k, int32_t* out, void* strea
 int spc_pin(spc_cache* c, int layer, int seq, int unit, const int32_t* positions, int npos,
             const void* k_rows, const void* v_rows, void* stream) {
   if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = check_not_pending(c, layer)) return rc;
   const Geo& G = c->G;
   cudaStream_t st = (cudaStream_t)stream;
   if (seq < 0 || seq >= G.batch || unit < 0 || unit >= G.U) return fail(SPC_EINVAL, "seq/unit out of range");
@@ -541,6 +575,7 @@ int spc_predecode_layer(spc_cache* c, int layer, const void* q, const void* k_ne
   if (int rc = check_layer(c, layer)) return rc;
   if (c->ticket[layer] != -1)
     return fail(SPC_EPROTO, "duplicate ticket for step 0 layer " + std::to_string(layer));
+  if (int rc = check_not_pending(c, layer)) return rc;
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));
@@ -556,6 +591,7 @@ int spc_decode_layer(spc_cache* c, int layer, int step, const void* q, const voi
   if (c->ticket[layer] != step - 1)  // transfer.py:96-100
     return fail(SPC_EPROTO, "no ticket was issued at step " + std::to_string(step - 1) + " for layer " +
                                 std::to_string(layer));
+  if (int rc = check_not_pending(c, layer)) return rc;
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
   cudaEvent_t w0 = nullptr, w1 = nullptr;
@@ -577,8 +613,36 @@ int spc_decode_layer(spc_cache* c, int layer, int step, const void* q, const voi
   return SPC_OK;
 }
 
+int spc_set_agg_reduce(spc_cache* c, int enable) {
+  if (!c) return fail(SPC_EINVAL, "null cache");
+  for (int l = 0; l < c->G.layers; ++l)
+    if (c->pend[l].on) return fail(SPC_EPROTO, "a layer is waiting for spc_finish_layer");
+  c->agg_ext = enable != 0;
+  return SPC_OK;
+}
+
+int spc_agg_buffer(spc_cache* c, int layer, float** agg, int64_t* count, void** stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  if (!c->agg_ext) return fail(SPC_EINVAL, "spc_agg_buffer needs spc_set_agg_reduce(cache, 1)");
+  if (agg) *agg = c->L[layer].agg;
+  if (count) *count = (int64_t)c->G.batch * c->G.U * c->G.L;
+  if (stream) *stream = (void*)c->cstream(layer);
+  return SPC_OK;
+}
+
+int spc_finish_layer(spc_cache* c, int layer) {
+  if (int rc = check_layer(c, layer)) return rc;
+  spc_cache::Pending& p = c->pend[layer];
+  if (!p.on)
+    return fail(SPC_EPROTO, "spc_finish_layer without a pending aggregate for layer " + std::to_string(layer));
+  CUDA_TRY(cudaSetDevice(c->device));
+  p.on = false;
+  return ticket_tail(c, layer, p.f, p.n_before, p.append, p.p0);
+}
+
 int spc_ticket(spc_cache* c, int layer, int32_t* picked, int32_t* new_count, void* stream) {
   if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = check_not_pending(c, layer)) return rc;
   const Geo& G = c->G;
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(c->device));
@@ -592,6 +656,7 @@ int spc_ticket(spc_cache* c, int layer, int32_t* picked, int32_t* new_count, voi
 
 int spc_debug_agg(spc_cache* c, int layer, float* agg, void* stream) {
   if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = check_not_pending(c, layer)) return rc;
   const Geo& G = c->G;
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));

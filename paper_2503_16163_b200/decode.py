@@ -50,9 +50,32 @@ class SpeculativeLayerDecoder:
     247-248, 288-289) per layer; ticket rules follow transfer.py:84-100 and are
     enforced by the C library (ProtocolError)."""
 
-    def __init__(self, cache: DeviceTwoTierCache):
+    def __init__(self, cache: DeviceTwoTierCache, agg_reduce=None):
+        """agg_reduce: for a KV-head-sharded cache with layer-scope top-k
+        (shard.py), a callable that sums a device fp32 tensor in place across
+        ranks (e.g. ``shard.allreduce_sum()``).  It is called on the cache's
+        copy stream after each layer's partial aggregate, before the top-k."""
         self.cache = cache
         self._dev = cache._torch_device
+        self._agg_reduce = agg_reduce
+        if agg_reduce is not None:
+            _lib.check(_lib.lib().spc_set_agg_reduce(cache.handle, 1))
+
+    def _finish(self, layer: int) -> None:
+        """Cross-rank sum of the partial aggregate, then the rest of the ticket."""
+        if self._agg_reduce is None:
+            return
+        import ctypes
+
+        import torch
+        lib = _lib.lib()
+        ptr, count, stream = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_void_p()
+        _lib.check(lib.spc_agg_buffer(self.cache.handle, layer, ctypes.byref(ptr), ctypes.byref(count),
+                                      ctypes.byref(stream)))
+        view = _device_f32(ptr.value, count.value, self._dev)
+        with torch.cuda.stream(torch.cuda.ExternalStream(stream.value, device=self._dev)):
+            self._agg_reduce(view)
+        _lib.check(lib.spc_finish_layer(self.cache.handle, layer))
 
     def _inputs(self, q, k_new, v_new, rows):
         c = self.cache
@@ -77,6 +100,7 @@ class SpeculativeLayerDecoder:
                                                   v.data_ptr(), out.data_ptr(),
                                                   current_stream(self._dev)))
         self._keep = (q, k, v)
+        self._finish(layer)
         return out
 
     def decode_layer(self, layer: int, step: int, q, k_new, v_new, out=None,
@@ -92,6 +116,7 @@ class SpeculativeLayerDecoder:
                                                v.data_ptr(), out.data_ptr(), pinned_mass.data_ptr(),
                                                current_stream(self._dev)))
         self._keep = (q, k, v)
+        self._finish(layer)
         return LayerResult(out, pinned_mass)
 
     def ticket(self, layer: int):
@@ -112,6 +137,19 @@ class SpeculativeLayerDecoder:
         agg = torch.empty((c.batch, c.units, L), dtype=torch.float32, device=self._dev)
         _lib.check(_lib.lib().spc_debug_agg(c.handle, layer, agg.data_ptr(), current_stream(self._dev)))
         return agg
+
+
+class _CudaArray:
+    """__cuda_array_interface__ over library-owned device memory (zero copy)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def _device_f32(ptr: int, count: int, device):
+    import torch
+    return torch.as_tensor(_CudaArray(ptr, count), device=device)
 
 
 def _capacity(c: DeviceTwoTierCache) -> int:

@@ -99,3 +99,74 @@ def test_plan_host_layers():
     assert cfg["layers"] % hl == 0 and hl * slab <= 0.45 * (196 << 30)
     assert bench.plan_host_layers(cfg, 8, avail=196 << 30) == 1
     assert bench.plan_host_layers(cfg, 1, avail=4 << 40) == 32
+
+
+# ---- KV-head sharding (shard.py): layer-scope top-k needs the agg all-reduce ----
+HCFG = dict(n0=300, H=4, Hq=8, d=16, bits=2, g=8, r=8, k=6)
+
+
+def _head_inputs():
+    rng = np.random.default_rng(7)
+    K, V = make_kv(rng, HCFG["n0"], HCFG["H"], HCFG["d"])
+    q = make_queries(rng, 2, HCFG["Hq"], HCFG["d"])
+    kn, vn = make_step_kv(rng, 2, HCFG["H"], HCFG["d"])
+    return K, V, q, kn, vn
+
+
+def _head_decode(rank, world):
+    from paper_2503_16163_b200.shard import head_shard
+    sh = head_shard(HCFG["H"], HCFG["Hq"], rank, world)
+    K, V, q, kn, vn = _head_inputs()
+    st = R.LayerState(sh.kv_heads, HCFG["d"], HCFG["bits"], HCFG["g"], HCFG["r"], HCFG["k"])
+    st.extend(sh.slice_kv(K), sh.slice_kv(V))
+    res = R.decode_layer(st, sh.slice_q(q), sh.slice_kv(kn), sh.slice_kv(vn))
+    return res, st.f
+
+
+def _head_worker(rank, port, out_q):
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    from paper_2503_16163_b200.shard import allreduce_sum
+    res, f = _head_decode(rank, WORLD)
+    agg = torch.from_numpy(np.ascontiguousarray(res["agg"][0], np.float32))   # this rank's partial
+    allreduce_sum()(agg)
+    picked = R.select_topk(agg.numpy(), HCFG["k"], range(f))
+    out_q.put((rank, res["out"], agg.numpy(), picked))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_head_sharding_layer_scope_allreduce():
+    """Each rank attends its half of the kv heads; the summed partial
+    aggregates select the same top-k as the single-process layer (engine.py:317)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_head_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    got = dict((r, rest) for r, *rest in (q.get(timeout=240) for _ in range(WORLD)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full, f = _head_decode(0, 1)
+    from paper_2503_16163_b200.shard import head_shard
+    for rank, (out, agg, picked) in got.items():
+        sh = head_shard(HCFG["H"], HCFG["Hq"], rank, WORLD)
+        np.testing.assert_array_equal(out, full["out"][:, sh.q_lo:sh.q_hi])
+        np.testing.assert_allclose(agg, full["agg"][0], rtol=1e-6, atol=1e-9)
+        assert picked == full["picked"][0]
+
+
+def test_head_shard_ranges():
+    from paper_2503_16163_b200.shard import head_shard
+    shards = [head_shard(8, 32, r, 4) for r in range(4)]
+    assert [(s.kv_lo, s.kv_hi, s.q_lo, s.q_hi) for s in shards] == [
+        (0, 2, 0, 8), (2, 4, 8, 16), (4, 6, 16, 24), (6, 8, 24, 32)]
+    assert all(s.q_heads == 4 * s.kv_heads for s in shards)   # GQA groups stay whole
+    with pytest.raises(ValueError):
+        head_shard(8, 32, 0, 3)      # heads run out -> shard by sequence instead
+    with pytest.raises(ValueError):
+        head_shard(8, 32, 4, 4)
