@@ -643,22 +643,31 @@ def run_full_decoder(args, cfg):
     rank, world, local, local_world = dist_env()
     torch.cuda.set_device(local)
     device = f"cuda:{local}"
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(device))
+    heads = args.shard == "heads"
+    if world > 1 or heads:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+        dist.init_process_group("nccl", device_id=torch.device(device), rank=rank, world_size=world)
     hidden, ffn, vocab = MODEL_SHAPES[args.config]
+    sh = None
+    if heads:  # attention heads split over the ranks, outputs all-gathered before Wo (decoder.py)
+        from paper_2503_16163_b200.shard import head_shard
+        sh = head_shard(cfg["kv_heads"], cfg["q_heads"], rank, world)
     sc = StackConfig(layers=cfg["layers"], q_heads=cfg["q_heads"], kv_heads=cfg["kv_heads"],
                      head_dim=cfg["head_dim"], hidden=hidden, ffn=ffn, vocab=vocab)
     W, K = args.warmup, args.steps
     host_layers = args.host_layers or plan_host_layers(cfg, local_world)
     budget = CacheBudget(bits=cfg["bits"], group_size=cfg["group"], residual=cfg["residual"],
                          prefetch_k=cfg["topk"], context_length=cfg["ctx"] + W + K + 64)
-    cache = DeviceTwoTierCache(cfg["layers"], cfg["kv_heads"], cfg["head_dim"], budget, batch=cfg["batch"],
-                               q_heads=cfg["q_heads"], device=local, host_layers=host_layers)
-    s0 = torch.randn((host_layers, cfg["batch"], cfg["q_heads"], cfg["head_dim"]), device=device).to(
+    lcfg = dict(cfg, kv_heads=sh.kv_heads, q_heads=sh.q_heads) if sh else cfg   # this rank's heads
+    cache = DeviceTwoTierCache(cfg["layers"], lcfg["kv_heads"], cfg["head_dim"], budget, batch=cfg["batch"],
+                               q_heads=lcfg["q_heads"], device=local, host_layers=host_layers)
+    s0 = torch.randn((host_layers, cfg["batch"], lcfg["q_heads"], cfg["head_dim"]), device=device).to(
         torch.bfloat16)
-    prefill_cache(cache, cfg, host_layers, s0, device, seed=99 + rank)
-    weights = random_stack(sc, device, seed=7 + rank)
-    stack = DecoderStack(sc, weights, cache)
+    prefill_cache(cache, lcfg, host_layers, s0, device, seed=99 + rank)
+    # head sharding: every rank holds the same (replicated) weights
+    weights = random_stack(sc, device, seed=7 + (0 if sh else rank))
+    stack = DecoderStack(sc, weights, cache, shard=sh)
     B, n = cfg["batch"], cfg["ctx"]
     gen = torch.Generator(device=device).manual_seed(5 + rank)
     tok0 = torch.randint(0, vocab, (B,), device=device, generator=gen)
@@ -686,21 +695,24 @@ def run_full_decoder(args, cfg):
     elapsed_ms = reduce_max(e0.elapsed_time(e1), device)
     prof = cache.profile(False)
     ms_per_step = elapsed_ms / K
-    tokens = whole_job_tokens(B, K, world)
+    tokens = B * K if heads else whole_job_tokens(B, K, world)
     value = tokens / (elapsed_ms / 1e3)
     f = cache.quantized_frontier(0)
     nn = cache.length(0)
-    kv_bytes = algorithmic_bytes_per_layer(cfg, nn - K // 2, f, cfg["topk"])["hbm"] * cfg["layers"]
+    kv_bytes = algorithmic_bytes_per_layer(lcfg, nn - K // 2, f, cfg["topk"])["hbm"] * cfg["layers"]
     wbytes = sc.weight_bytes()
     achieved = (kv_bytes + wbytes) / (ms_per_step / 1e3) / 1e9
     peak, peak_src = hbm_peak()
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if heads else "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic prompt KV + random-init weights; tokens fed back on device",
         "config": {"workload": cfg["workload"] + f"; FULL DECODER (hidden {hidden}, ffn {ffn}, vocab {vocab})",
-                   "global_batch": B * world, "seq_len": n, "layers": cfg["layers"],
-                   "parallelism": f"replicas-by-sequence x{world} (no collective)", "host_layers": host_layers,
+                   "global_batch": B * (1 if heads else world), "seq_len": n, "layers": cfg["layers"],
+                   "parallelism": (f"kv-heads x{world} (attention outputs all-gathered before Wo; Wo/FFN/head "
+                                   "replicated; agg all-reduce per layer)") if heads
+                   else f"replicas-by-sequence x{world} (no collective)", "host_layers": host_layers,
                    "l2": "no flush: weights %.1f GB + KV %.1f GB per step >> L2" % (wbytes / 1e9, kv_bytes / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_src, "kernel": "whole step (KV + weights)",
@@ -718,7 +730,7 @@ def run_full_decoder(args, cfg):
     if rank == 0:
         print(json.dumps(line), flush=True)
     cache.close()
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 

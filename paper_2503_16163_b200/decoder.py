@@ -14,6 +14,13 @@ the B200, so tokens/s can be timed with the weight traffic included:
 Residual stream fp32; GEMM operands bf16 with fp32 accumulation (cuBLAS);
 weights stored [out, in] so every GEMM is x @ W^T.  Batch sharding (bench.py)
 keeps this exchange-free, so there is no all-gather on this path.
+
+KV-head sharding (``shard=HeadShard``, shard.py; SURVEY 8(e) collective (3)):
+the rank projects and attends only its heads (its rows of Wq|Wk|Wv, its cache
+shard), the per-head attention outputs are all-gathered across ranks (NCCL
+over NVLink on a multi-GPU box) into the head order Wo expects, and Wo, the
+FFN and the logits run replicated.  Layer-scope top-k reduces the partial
+aggregates as in decode.SpeculativeLayerDecoder.
 """
 from __future__ import annotations
 
@@ -99,12 +106,31 @@ def stack_from_reference(cfg, weights, device="cuda:0") -> tuple[StackConfig, St
                             head=bf(weights.head.T))
 
 
+def _shard_weights(cfg: StackConfig, w: StackWeights, sh) -> StackWeights:
+    """Rows of Wq|Wk|Wv for this rank's q and kv heads; everything else shared."""
+    import torch
+    d, qd, kd = cfg.head_dim, cfg.q_heads * cfg.head_dim, cfg.kv_heads * cfg.head_dim
+    layers = []
+    for lw in w.layers:
+        wq, wk, wv = lw["wqkv"][:qd], lw["wqkv"][qd:qd + kd], lw["wqkv"][qd + kd:]
+        wqkv = torch.cat([wq[sh.q_lo * d:sh.q_hi * d], wk[sh.kv_lo * d:sh.kv_hi * d],
+                          wv[sh.kv_lo * d:sh.kv_hi * d]]).contiguous()
+        layers.append({**lw, "wqkv": wqkv})
+    return StackWeights(emb=w.emb, layers=layers, final_norm=w.final_norm, head=w.head)
+
+
 class DecoderStack:
     """Decode steps of the whole model over a DeviceTwoTierCache (one per
     batch of sequences).  Preallocated buffers, no host syncs inside a step."""
 
-    def __init__(self, cfg: StackConfig, weights: StackWeights, cache: DeviceTwoTierCache):
+    def __init__(self, cfg: StackConfig, weights: StackWeights, cache: DeviceTwoTierCache,
+                 shard=None, group=None):
         import torch
+        self.shard, self.group = shard, group
+        self.full_q_heads = cfg.q_heads
+        if shard is not None:  # this rank's heads; weights arrive whole and are sliced here
+            weights = _shard_weights(cfg, weights, shard)
+            cfg = StackConfig(**{**cfg.__dict__, "q_heads": shard.q_heads, "kv_heads": shard.kv_heads})
         if (cache.layers, cache.kv_heads, cache.head_dim, cache.q_heads) != (
                 cfg.layers, cfg.kv_heads, cfg.head_dim, cfg.q_heads):
             raise ValueError("cache geometry does not match the decoder")
@@ -134,6 +160,15 @@ class DecoderStack:
         self.pos = e(R, dt=i32)
         self.rope = e(R, cfg.head_dim, dt=f32)  # (cos, sin) per (row, pair)
         self.pinned_mass = e(B, cfg.q_heads, dt=f32)
+        if shard is not None:
+            W = shard.world
+            self.attn_all = e(W, R, cfg.q_heads * cfg.head_dim)            # all-gather target
+            self.attn_cat = e(R, self.full_q_heads * cfg.head_dim)         # [row][rank][head][d]
+            self._agg = None
+            if cache.topk_scope == "layer":
+                from .decode import SpeculativeLayerDecoder
+                from .shard import allreduce_sum
+                self._agg = SpeculativeLayerDecoder(cache, agg_reduce=allreduce_sum(group))
         self.launches = 0  # kernels + GEMMs this object issued outside spc_decode_layer
 
     def _layers(self, rows: int, step: int | None) -> None:
@@ -161,7 +196,12 @@ class DecoderStack:
             else:
                 _lib.check(lib.spc_decode_layer(h, layer, step, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                                 attn.data_ptr(), self.pinned_mass.data_ptr(), st))
-            torch.matmul(attn.view(rows, -1), lw["wo"].t(), out=delta)
+            if self.shard is not None:
+                if self._agg is not None:
+                    self._agg._finish(layer)
+                torch.matmul(self._gather_heads(attn, rows), lw["wo"].t(), out=delta)
+            else:
+                torch.matmul(attn.view(rows, -1), lw["wo"].t(), out=delta)
             _lib.check(lib.spc_add_rmsnorm(x.data_ptr(), delta.data_ptr(), lw["ffn_norm"].data_ptr(),
                                            xn.data_ptr(), rows, cfg.hidden, cfg.eps, st))
             torch.matmul(xn, lw["w1"].t(), out=g)
@@ -173,6 +213,24 @@ class DecoderStack:
         torch.matmul(xn, self.w.head.t(), out=logits)
         _lib.check(lib.spc_argmax_rows(logits.data_ptr(), rows, cfg.vocab, self.next.data_ptr(), st))
         self.launches += len(self.w.layers) * 8 + 4
+
+    def _gather_heads(self, attn, rows: int):
+        """All-gather of the per-head attention outputs of every rank, laid out
+        [row][all q heads][d] for Wo (ranks own contiguous head ranges)."""
+        import torch
+        import torch.distributed as dist
+        W = self.shard.world
+        src = attn.view(rows, -1)
+        dst = self.attn_all[:, :rows]
+        if W == 1:
+            dst[0].copy_(src)
+        elif dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(dst, src, group=self.group)
+        else:  # gloo (CPU-side / single-GPU multi-process tests)
+            dist.all_gather(list(dst.unbind(0)), src.contiguous(), group=self.group)
+        cat = self.attn_cat[:rows]
+        cat.view(rows, W, -1).copy_(dst.transpose(0, 1))
+        return cat
 
     def _embed(self, tokens, rows: int) -> None:
         import torch

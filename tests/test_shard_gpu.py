@@ -173,3 +173,74 @@ def test_agg_reduce_protocol():
     torch.cuda.synchronize()
     assert (picked >= 0).sum().item() == 16
     cache.close()
+
+
+# ---- the full decoder step with head-sharded attention + all-gather of the outputs ----
+def _stack_run(rank, world, group=None):
+    """Predecode + 3 decode steps of a 2-layer GQA model (8 q / 2 kv heads) with
+    fixed token inputs; returns the logits of every call (numpy)."""
+    import torch
+    from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
+    from paper_2503_16163_b200.decoder import DecoderStack, stack_from_reference
+    from paper_2503_16163_b200.shard import head_shard
+    from paper_2503_16163_b200.weights import DecoderConfig, init_decoder
+    torch.backends.cuda.matmul.allow_tf32 = False
+    rc = DecoderConfig(layers=2, q_heads=8, kv_heads=2, head_dim=128, vocab=512, hidden=256, ffn=512, seed=4)
+    cfg, W = stack_from_reference(rc, init_decoder(rc))
+    sh = head_shard(cfg.kv_heads, cfg.q_heads, rank, world) if world > 1 else None
+    B, n0 = 3, 400
+    budget = CacheBudget(bits=2, group_size=32, residual=64, prefetch_k=16, context_length=1024)
+    kvh, qh = (sh.kv_heads, sh.q_heads) if sh else (cfg.kv_heads, cfg.q_heads)
+    cache = DeviceTwoTierCache(cfg.layers, kvh, cfg.head_dim, budget, batch=B, q_heads=qh)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for layer in range(cfg.layers):
+        K = torch.randn(B, n0, cfg.kv_heads, cfg.head_dim, device="cuda", generator=g).bfloat16()
+        V = torch.randn(B, n0, cfg.kv_heads, cfg.head_dim, device="cuda", generator=g).bfloat16()
+        if sh:
+            K, V = sh.slice_kv(K).contiguous(), sh.slice_kv(V).contiguous()
+        cache.prefill(layer, K, V)
+    stack = DecoderStack(cfg, W, cache, shard=sh, group=group)
+    tok = torch.randint(0, cfg.vocab, (B,), device="cuda", generator=g)
+    pos = torch.full((B,), n0, dtype=torch.int32, device="cuda")
+    stack.predecode(tok, pos)
+    logits = [stack.logits[:B].float().cpu().numpy()]
+    for step in range(1, 4):
+        toks = torch.randint(0, cfg.vocab, (B, 2), device="cuda", generator=g)
+        stack.decode_step(step, toks, pos)
+        logits.append(stack.logits.float().cpu().numpy())
+        pos = pos + 1
+    cache.close()
+    return logits
+
+
+def _stack_worker(rank, port, out_q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        out_q.put((rank, _stack_run(rank, WORLD)))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_head_sharded_decoder_stack_matches_single_process():
+    """Each rank projects and attends its heads; the all-gathered outputs feed a
+    replicated Wo / FFN / head, so every rank's logits match the single-GPU stack."""
+    import torch.multiprocessing as mp
+    full = _stack_run(0, 1)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stack_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=400) for _ in range(WORLD))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for i, ref in enumerate(full):
+        np.testing.assert_array_equal(got[0][i], got[1][i])        # replicated after the all-gather
+        scale = np.abs(ref).max()
+        assert np.abs(got[0][i] - ref).max() <= 2e-2 * scale, (i, np.abs(got[0][i] - ref).max() / scale)
