@@ -438,3 +438,22 @@ def test_extreme_magnitudes(kscale, vscale, tau):
         assert_topk_equivalent(picked, list(o["picked"][0]), o["agg"][0], k)
         st.pinned[0] = tuple(sorted(picked))
     cache.close()
+
+
+@pytest.mark.parametrize("bits,H,Hq", [(2, 4, 4), (1, 2, 8)])
+def test_group_64_vs_oracle(bits, H, Hq):
+    """g=64 (the paper's Table 4 setting, SURVEY 8 "g=64 sweep"): 64-token key
+    groups and 64-channel value groups, on the generic exact kernel."""
+    _oracle_run((2, 1400, H, Hq, 128, bits, 64, 64, 32, "layer"), seed=41 + bits)
+
+
+def test_4bit_vs_oracle():
+    """4-bit codes (CacheBudget allows bits in {1, 2, 4, 16}; generic kernel)."""
+    _oracle_run((2, 900, 2, 8, 128, 4, 32, 64, 24, "layer"), seed=45)
+
+
+@pytest.mark.parametrize("d", [64, 80])
+def test_other_head_dims_vs_oracle(d):
+    """Head dims other than 128 take the generic kernel; g=32 value groups with
+    a ragged last group (16 channels) at d=80 (quant.py per-token groups, test_quant.py:149-154)."""
+    _oracle_run((2, 700, 2, 4, d, 2, 32, 32, 16, "layer"), seed=47)
