@@ -125,7 +125,7 @@ int check_not_pending(const spc_cache* c, int layer) {
 
 void choose_splits(const spc_cache* c, int f, int* nsplit, int* bps) {
   const Geo& G = c->G;
-  int nblk = f / G.g;
+  int nblk = f / G.tb;
   if (nblk <= 0) {
     *nsplit = 1;
     *bps = 1;
@@ -343,14 +343,16 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
   int lcm = G.g;
   while (lcm % 32) lcm += G.g;
   G.L = (int)align_up((size_t)d->context_length, (size_t)lcm);
-  G.nblk = G.L / G.g;
   G.ring = G.r + G.g;
   G.nch = (G.d + G.g - 1) / G.g;
   G.krw = G.bits == 16 ? G.d / 2 : (G.d * G.bits + 31) / 32;
   G.vrw = G.krw;
-  G.fast = (G.d == 128 && G.g == 32 && (G.bits == 1 || G.bits == 2)) ? 1 : 0;
-  G.bwords = G.g * G.krw;
-  G.rec = 2 * G.bwords + (G.bits == 16 ? 0 : G.d + G.g * G.nch);
+  G.fast = (G.d == 128 && (G.g == 32 || G.g == 64) && (G.bits == 1 || G.bits == 2)) ? 1 : 0;
+  G.tb = G.fast ? 32 : G.g;
+  G.vps = G.fast ? G.d / 32 : G.nch;
+  G.nblk = G.L / G.tb;
+  G.bwords = G.tb * G.krw;
+  G.rec = 2 * G.bwords + (G.bits == 16 ? 0 : G.d + G.tb * G.vps);
 
   int rc = SPC_OK;
   const size_t b = G.batch, H = G.H, U = G.U;
@@ -361,7 +363,7 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
     size_t kpar = 0, vpar = 0;
     size_t ring = b * H * G.ring * (size_t)G.d * 2;
     size_t pool = b * U * G.k * (size_t)G.Hu * G.d * 2;
-    size_t off[16], tot = 0, sizes[16] = {codes, codes, kpar, vpar, ring, ring, pool, pool,
+    size_t off[16], tot = 0, sizes[16] = {codes, 0, kpar, vpar, ring, ring, pool, pool,
                                           b * U * G.k * 4, b * U * (G.L / 32) * 4, b * U * (size_t)G.L * 4,
                                           b * U * G.k * 4, b * U * 4, b * U * G.k * 4, b * U * G.k * 4,
                                           b * H * 2 * 4};

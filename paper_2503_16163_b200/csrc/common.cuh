@@ -2,17 +2,22 @@
 // every kernel of the SpeCache decode path (sm_100a).
 //
 // HBM layout per (layer) -- blocks are [seq][kv head][block] records of G.rec
-// words, one contiguous record per g-token block so a block moves with a single
-// bulk copy; within a record (pointers kcodes/vcodes/kparams/vparams are the
-// field bases, the block stride is G.rec for all four):
-//   kcodes  uint32 [g][krw]               key codes, token-major rows, LSB-first
-//                                         channel order (the reference's key
-//                                         group is a column of this block)
-//   vcodes  uint32 [g*vrw]                value codes; token-major rows in the
+// words, one contiguous record per tb-token block so a block moves with a
+// single bulk copy.  tb = g in the generic layout; the fast layout (d=128,
+// bits 1|2) always uses 32-token records, and for g=64 each 64-token group
+// spans two records that both carry its key params, while every 32-channel
+// value slot carries the params of the 64-channel group containing it (the
+// MMA kernel is then the same for g=32 and g=64).  Within a record (pointers
+// kcodes/vcodes/kparams/vparams are the field bases, the block stride is G.rec
+// for all four):
+//   kcodes  uint32 [tb][krw]              key codes, token-major rows, LSB-first
+//                                         channel order (a key group is a column
+//                                         of the g/tb records of its group)
+//   vcodes  uint32 [tb*vrw]               value codes; token-major rows in the
 //                                         generic layout, MMA-fragment-native in
 //                                         the fast layout (see vloc)
 //   kparams uint32 [d]                    bf16 (lo | hi<<16) per key group (kpi)
-//   vparams uint32 [g*nch]                bf16 (lo | hi<<16) per value group (vpi)
+//   vparams uint32 [tb*vps]               bf16 (lo | hi<<16) per value slot (vpi)
 //   ring_k/v bf16  [b][H][r+g][d]         residual window, slot = pos % (r+g)
 //   pool_k/v bf16  [b][U][k][Hu][d]       pinned full-precision rows (slots)
 //   pin_pos int32  [b][U][k]              position held by each slot (-1 empty)
@@ -36,13 +41,15 @@ struct Geo {
   int G;      // q heads per kv head
   int U;      // top-k units per (seq, layer): 1 (layer scope) or H
   int Hu;     // kv heads per unit
-  int nblk;   // packed blocks per (seq, head): L / g
+  int nblk;   // block records per (seq, head): L / tb
   int ring;   // r + g
   int nch;    // value groups per token: ceil(d / g)
   int krw;    // uint32 words per key-code row
   int vrw;    // uint32 words per value-code row (generic) / per block = g*vrw
-  int fast;   // fast MMA layout (d=128, g=32, bits 1|2)
-  int bwords; // uint32 words of (key or value) codes per block = g*krw
+  int fast;   // fast MMA layout (d=128, g=32|64, bits 1|2)
+  int tb;     // tokens per block record: g (generic) / 32 (fast)
+  int vps;    // value param words per token in a record: nch (generic) / d/32 (fast)
+  int bwords; // uint32 words of (key or value) codes per record = tb*krw
   int rec;    // uint32 words per block record [kcodes | vcodes | kparams | vparams]
 };
 
@@ -206,6 +213,12 @@ __host__ __device__ inline int vpi(const Geo& G, int t, int j) {
   const int ks = t >> 4, khalf = (t >> 3) & 1, tq = (t >> 1) & 3, odd = t & 1;
   return 32 * j + 8 * tq + 4 * ks + 2 * khalf + odd;
 }
+
+// Value-param slot of channel c within a token's record words, and the first
+// slot of value group j (the fast layout repeats a g=64 group's params in both
+// of its 32-channel slots).
+__host__ __device__ inline int vslot(const Geo& G, int c) { return G.fast ? (c >> 5) : c / G.g; }
+__host__ __device__ inline int vslot_of_group(const Geo& G, int j) { return G.fast ? j * (G.g >> 5) : j; }
 
 __device__ inline uint32_t read_code(const uint32_t* blk_words, int word, int bit, int bits) {
   return (blk_words[word] >> bit) & ((1u << bits) - 1u);

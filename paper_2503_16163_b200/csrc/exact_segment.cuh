@@ -32,7 +32,7 @@ __device__ inline float dq_val(const Geo& G, const LayerBufs& B, size_t bi, int 
   vloc(G, t, c, &w, &bit);
   uint32_t code = read_code(B.vcodes + bi * (size_t)G.rec, w, bit, G.bits);
   return dequant_exact(code, params_from_word(
-      B.vparams[bi * (size_t)G.rec + vpi(G, t, c / G.g)], G.bits));
+      B.vparams[bi * (size_t)G.rec + vpi(G, t, vslot(G, c))], G.bits));
 }
 
 // One CTA (kCH threads, named barrier 1) of the exact path for (split, h, b).
@@ -86,9 +86,9 @@ __device__ __forceinline__ void generic_cta(const AttnArgs& a, const int split, 
     total = npin + nres + a.rows;
   } else {
     int blk0 = split * a.blocks_per_split;
-    int blk1 = min(blk0 + a.blocks_per_split, a.f / G.g);
-    begin = blk0 * G.g;
-    total = max(0, blk1 - blk0) * G.g;
+    int blk1 = min(blk0 + a.blocks_per_split, a.f / G.tb);
+    begin = blk0 * G.tb;
+    total = max(0, blk1 - blk0) * G.tb;
   }
 
   float pin_m[kMaxR], pin_l[kMaxR];
@@ -113,8 +113,8 @@ __device__ __forceinline__ void generic_cta(const AttnArgs& a, const int split, 
         if (!exact_seg) {
           pos = begin + it;
           masked_all = (bitmap[pos >> 5] >> (pos & 31)) & 1u;
-          int blk = pos / G.g;
-          tb = pos - blk * G.g;
+          int blk = pos / G.tb;
+          tb = pos - blk * G.tb;
           bi = blk_index(G, b, h, blk);
         } else if (it < npin) {
           int slot = slots[it];
@@ -201,8 +201,8 @@ __device__ __forceinline__ void generic_cta(const AttnArgs& a, const int split, 
           if (!exact_seg) {
             int pos = begin + it;
             if ((bitmap[pos >> 5] >> (pos & 31)) & 1u) continue;  // p == 0
-            int blk = pos / G.g;
-            vv = dq_val(G, B, blk_index(G, b, h, blk), pos - blk * G.g, c);
+            int blk = pos / G.tb;
+            vv = dq_val(G, B, blk_index(G, b, h, blk), pos - blk * G.tb, c);
           } else if (it < npin) {
             int slot = slots[it];
             vv = __bfloat162float(B.pool_v[((((size_t)b * G.U + unit) * G.k + slot) * G.Hu + hh) * d + c]);

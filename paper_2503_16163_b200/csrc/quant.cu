@@ -11,20 +11,22 @@
 
 namespace spc {
 
-// One CTA quantizes one g-token block of one (seq, kv head).  The block is
-// staged in shared memory as fp32 (exact copies of the bf16 inputs), group
-// (min, max) are reduced there, codes are computed in float64 exactly as the
-// reference does and OR-ed into the block's packed words in shared memory,
-// then the words stream out coalesced.
+// One CTA quantizes one g-token group of one (seq, kv head) -- R = g/tb block
+// records (R = 1 except the fast layout at g=64).  The group is staged in
+// shared memory as fp32 (exact copies of the bf16 inputs), group (min, max)
+// are reduced there, codes are computed in float64 exactly as the reference
+// does and OR-ed into the records' packed words in shared memory, then the
+// words stream out coalesced.
 __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S, int blk0) {
   const int blk = blk0 + blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int g = G.g, d = G.d, tid = threadIdx.x, nt = blockDim.x;
+  const int R = g / G.tb, nw = R * G.bwords;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* sk = reinterpret_cast<float*>(smem_raw);            // [g][d]
   float* sv = sk + g * d;                                    // [g][d]
-  uint32_t* wk = reinterpret_cast<uint32_t*>(sv + g * d);    // [g*krw]
-  uint32_t* wv = wk + G.bwords;                              // [g*vrw]
-  double* kz = reinterpret_cast<double*>(wv + G.bwords + (G.bwords & 1));  // [d]
+  uint32_t* wk = reinterpret_cast<uint32_t*>(sv + g * d);    // [R][tb*krw]
+  uint32_t* wv = wk + nw;                                    // [R][tb*vrw]
+  double* kz = reinterpret_cast<double*>(wv + nw + (nw & 1));  // [d]
   double* ks = kz + d;
   double* vz = ks + d;                                       // [g][nch]
   double* vs = vz + g * G.nch;
@@ -38,7 +40,7 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
     sv[i] = __bfloat162float(S.v[off]);
   }
   __syncthreads();
-  const size_t bi = blk_index(G, b, h, blk);
+  const size_t bi = blk_index(G, b, h, blk * R);  // first record of the group
 
   if (G.bits == 16) {  // verbatim full-precision tier (kvcache.py:185-187)
     __nv_bfloat16* okc = reinterpret_cast<__nv_bfloat16*>(B.kcodes + bi * (size_t)G.rec);
@@ -64,7 +66,8 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
       lo = fminf(lo, x);
       hi = fmaxf(hi, x);
     }
-    B.kparams[bi * G.rec + kpi(G, c)] = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+    const uint32_t pw = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+    for (int r = 0; r < R; ++r) B.kparams[(bi + r) * G.rec + kpi(G, c)] = pw;  // every record of the group
     atomicMax(reinterpret_cast<unsigned*>(&s_rk), __float_as_uint(hi - lo));
     GroupParams p = params_from_minmax((double)lo, (double)hi, G.bits);
     kz[c] = p.zero;
@@ -80,14 +83,15 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
       lo = fminf(lo, x);
       hi = fmaxf(hi, x);
     }
-    B.vparams[bi * (size_t)G.rec + vpi(G, t, j)] =
-        float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+    const uint32_t pw = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+    const int r = t / G.tb, tt = t - r * G.tb, s0 = vslot_of_group(G, j), s1 = vslot_of_group(G, j + 1);
+    for (int sl = s0; sl < s1 && sl < G.vps; ++sl) B.vparams[(bi + r) * (size_t)G.rec + vpi(G, tt, sl)] = pw;
     atomicMax(reinterpret_cast<unsigned*>(&s_rv), __float_as_uint(hi - lo));
     GroupParams p = params_from_minmax((double)lo, (double)hi, G.bits);
     vz[i] = p.zero;
     vs[i] = p.scale;
   }
-  for (int i = tid; i < G.bwords; i += nt) {
+  for (int i = tid; i < nw; i += nt) {
     wk[i] = 0u;
     wv[i] = 0u;
   }
@@ -98,22 +102,25 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
   }
   for (int i = tid; i < g * d; i += nt) {
     int t = i / d, c = i - t * d, w, bit;
+    const int r = t / G.tb, tt = t - r * G.tb;
     GroupParams pk{kz[c], ks[c]};
     uint32_t ck = quantize_code(sk[i], pk, G.bits);
-    kloc(G, t, c, &w, &bit);
-    if (ck) atomicOr(&wk[w], ck << bit);
+    kloc(G, tt, c, &w, &bit);
+    if (ck) atomicOr(&wk[r * G.bwords + w], ck << bit);
     int j = c / g;
     GroupParams pv{vz[t * G.nch + j], vs[t * G.nch + j]};
     uint32_t cv = quantize_code(sv[i], pv, G.bits);
-    vloc(G, t, c, &w, &bit);
-    if (cv) atomicOr(&wv[w], cv << bit);
+    vloc(G, tt, c, &w, &bit);
+    if (cv) atomicOr(&wv[r * G.bwords + w], cv << bit);
   }
   __syncthreads();
-  uint32_t* okc = B.kcodes + bi * (size_t)G.rec;
-  uint32_t* ovc = B.vcodes + bi * (size_t)G.rec;
-  for (int i = tid; i < G.bwords; i += nt) {
-    okc[i] = wk[i];
-    ovc[i] = wv[i];
+  for (int r = 0; r < R; ++r) {
+    uint32_t* okc = B.kcodes + (bi + r) * (size_t)G.rec;
+    uint32_t* ovc = B.vcodes + (bi + r) * (size_t)G.rec;
+    for (int i = tid; i < G.bwords; i += nt) {
+      okc[i] = wk[r * G.bwords + i];
+      ovc[i] = wv[r * G.bwords + i];
+    }
   }
 }
 
@@ -307,7 +314,7 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
 
 size_t quantize_smem_bytes(const Geo& G) {
   size_t s = 2 * sizeof(float) * G.g * G.d;
-  s += sizeof(uint32_t) * (2 * G.bwords + 2);
+  s += sizeof(uint32_t) * (2 * (G.g / G.tb) * G.bwords + 2);
   s += sizeof(double) * (2 * G.d + 2 * G.g * G.nch);
   return s;
 }
@@ -336,11 +343,13 @@ void launch_quantize(const Geo& G, const LayerBufs& B, const QuantSrc& S, int bl
 __global__ void k_export(Geo G, LayerBufs B, int seq, int nblocks, uint8_t* kcodes,
                          uint16_t* kzero, uint16_t* kscale, uint8_t* vcodes, uint16_t* vzero,
                          uint16_t* vscale) {
-  const int blk = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
+  const int blk = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;   // blk: g-token group
   const int g = G.g, d = G.d, bits = G.bits, nb = (g * bits + 7) / 8;
-  const size_t bi = blk_index(G, seq, h, blk);
-  const uint32_t* kw = B.kcodes + bi * (size_t)G.rec;
-  const uint32_t* vw = B.vcodes + bi * (size_t)G.rec;
+  const int R = g / G.tb;
+  const size_t bi = blk_index(G, seq, h, blk * R);   // the group's first record
+  // token t of the group: record t / tb, row t % tb
+  auto kw_of = [&](int t) { return B.kcodes + (bi + t / G.tb) * (size_t)G.rec; };
+  auto vw_of = [&](int t) { return B.vcodes + (bi + t / G.tb) * (size_t)G.rec; };
   const int per = 8 / bits;
   // key groups [nblocks][H][d][nb]
   for (int i = tid; i < d * nb; i += blockDim.x) {
@@ -350,8 +359,8 @@ __global__ void k_export(Geo G, LayerBufs B, int seq, int nblocks, uint8_t* kcod
       int t = byte * per + j;
       if (t >= g) break;
       int w, bit;
-      kloc(G, t, c, &w, &bit);
-      v |= read_code(kw, w, bit, bits) << (j * bits);
+      kloc(G, t % G.tb, c, &w, &bit);
+      v |= read_code(kw_of(t), w, bit, bits) << (j * bits);
     }
     kcodes[(((size_t)blk * G.H + h) * d + c) * nb + byte] = (uint8_t)v;
   }
@@ -369,14 +378,15 @@ __global__ void k_export(Geo G, LayerBufs B, int seq, int nblocks, uint8_t* kcod
       int c = j * g + byte * per + jj;
       if (c >= min(d, (j + 1) * g)) break;
       int w, bit;
-      vloc(G, t, c, &w, &bit);
-      v |= read_code(vw, w, bit, bits) << (jj * bits);
+      vloc(G, t % G.tb, c, &w, &bit);
+      v |= read_code(vw_of(t), w, bit, bits) << (jj * bits);
     }
     vcodes[((((size_t)blk * g + t) * G.H + h) * G.nch + j) * nb + byte] = (uint8_t)v;
   }
   for (int i = tid; i < g * G.nch; i += blockDim.x) {
     int t = i / G.nch, j = i - t * G.nch;
-    GroupParams p = params_from_word(B.vparams[bi * (size_t)G.rec + vpi(G, t, j)], bits);
+    GroupParams p = params_from_word(
+        B.vparams[(bi + t / G.tb) * (size_t)G.rec + vpi(G, t % G.tb, vslot_of_group(G, j))], bits);
     size_t o = (((size_t)blk * g + t) * G.H + h) * G.nch + j;
     vzero[o] = double_to_half_bits_rn(p.zero);
     vscale[o] = double_to_half_bits_rn(p.scale);
@@ -394,7 +404,7 @@ void launch_export(const Geo& G, const LayerBufs& B, int seq, int nblocks, uint8
 // Exact materialize of one (seq, head): float32 [n][d] keys and values,
 // bit-identical to TwoTierCache.materialize (kvcache.py:222-243).
 __device__ inline float packed_key(const Geo& G, const LayerBufs& B, int b, int h, int pos, int c) {
-  int blk = pos / G.g, t = pos - blk * G.g;
+  int blk = pos / G.tb, t = pos - blk * G.tb;
   size_t bi = blk_index(G, b, h, blk);
   if (G.bits == 16)
     return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B.kcodes + bi * (size_t)G.rec)[t * G.d + c]);
@@ -404,14 +414,14 @@ __device__ inline float packed_key(const Geo& G, const LayerBufs& B, int b, int 
   return dequant_exact(code, params_from_word(B.kparams[bi * G.rec + kpi(G, c)], G.bits));
 }
 __device__ inline float packed_val(const Geo& G, const LayerBufs& B, int b, int h, int pos, int c) {
-  int blk = pos / G.g, t = pos - blk * G.g;
+  int blk = pos / G.tb, t = pos - blk * G.tb;
   size_t bi = blk_index(G, b, h, blk);
   if (G.bits == 16)
     return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B.vcodes + bi * (size_t)G.rec)[t * G.d + c]);
   int w, bit;
   vloc(G, t, c, &w, &bit);
   uint32_t code = read_code(B.vcodes + bi * (size_t)G.rec, w, bit, G.bits);
-  return dequant_exact(code, params_from_word(B.vparams[bi * (size_t)G.rec + vpi(G, t, c / G.g)], G.bits));
+  return dequant_exact(code, params_from_word(B.vparams[bi * (size_t)G.rec + vpi(G, t, vslot(G, c))], G.bits));
 }
 
 __global__ void k_materialize(Geo G, LayerBufs B, int b, int h, int n, int f, float* keys,

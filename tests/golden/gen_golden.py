@@ -362,6 +362,13 @@ def gen_hitrate():
         json.dump({"args": args, "report": rep}, fh, indent=1)
 
 
+def gen_g64():
+    """g=64 (the paper's Table 4 group size): the fast layout's two-record groups."""
+    gen_cache("b2_d128_g64", 2, 2, 128, 64, 64, 8, 330, [0, 5, 100, 200], seed=21)
+    gen_cache("b1_d128_g64", 1, 2, 128, 64, 64, 8, 330, [3, 64, 191], seed=22)
+    gen_decode("gqa_b2_g64", 2, 8, 2, 128, 64, 64, 16, 400, 3, seed=23)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
     os.chdir(HERE)
     for name in sys.argv[1:]:

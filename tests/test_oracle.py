@@ -51,7 +51,7 @@ def test_frontier_rule():
 
 
 @pytest.mark.parametrize("tag", ["b2_d128", "b1_d128", "b4_d128", "b16_d128",
-                                 "b2_d10_g4", "b1_d8_g4"])
+                                 "b2_d10_g4", "b1_d8_g4", "b2_d128_g64", "b1_d128_g64"])
 def test_snapshot_and_materialize_match_reference(tag):
     c = golden(f"cache_{tag}.npz")
     K, V, bits, g, r = c["K"], c["V"], int(c["bits"]), int(c["g"]), int(c["r"])
@@ -70,7 +70,7 @@ def test_snapshot_and_materialize_match_reference(tag):
     assert np.array_equal(mv.view(np.uint32), c["mat_v"].view(np.uint32))
 
 
-@pytest.mark.parametrize("tag", ["mha_b2", "gqa_b1", "mha_b16", "gqa4_b2"])
+@pytest.mark.parametrize("tag", ["mha_b2", "gqa_b1", "mha_b16", "gqa4_b2", "gqa_b2_g64"])
 def test_decode_layer_matches_reference(tag):
     z = golden(f"decode_{tag}.npz")
     bits, g, r, k, Hq = (int(z[x]) for x in ("bits", "g", "r", "k", "Hq"))

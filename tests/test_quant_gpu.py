@@ -9,7 +9,7 @@ from oracle.synth import make_kv
 
 pytestmark = pytest.mark.gpu
 
-TAGS = ["b2_d128", "b1_d128", "b4_d128", "b16_d128", "b2_d10_g4", "b1_d8_g4"]
+TAGS = ["b2_d128", "b1_d128", "b4_d128", "b16_d128", "b2_d10_g4", "b1_d8_g4", "b2_d128_g64", "b1_d128_g64"]
 
 
 def _cache(c, mode, batch=1):

@@ -8,7 +8,7 @@ decode steps with the library's live CUDA-event profiling.  Reports per point:
   fraction of the measured HBM peak, and K5 (PCIe prefetch) GB/s = bytes the
   gathers moved / their kernel time.
 
-  python tools/sweep.py [--quick] > gpurun_out/sweep.jsonl
+  python tools/sweep.py [--quick] [--group 64] [--ctx ...] [--topk ...] > gpurun_out/sweep.jsonl
 """
 import argparse
 import ctypes
@@ -20,7 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def point(bits, ctx, k, steps=10, warmup=3):
+def point(bits, ctx, k, steps=10, warmup=3, group=32):
     import torch
 
     import bench
@@ -28,9 +28,9 @@ def point(bits, ctx, k, steps=10, warmup=3):
 
     batch = max(1, min(16, (1 << 19) // ctx))
     cfg = dict(workload=f"sweep bits={bits} ctx={ctx} k={k}", layers=1, batch=batch, kv_heads=32,
-               q_heads=32, head_dim=128, ctx=ctx, bits=bits, group=32, residual=64, topk=k)
+               q_heads=32, head_dim=128, ctx=ctx, bits=bits, group=group, residual=64, topk=k)
     dev = "cuda:0"
-    budget = CacheBudget(bits=bits, group_size=32, residual=64, prefetch_k=k,
+    budget = CacheBudget(bits=bits, group_size=group, residual=64, prefetch_k=k,
                          context_length=ctx + steps + warmup + 64)
     cache = DeviceTwoTierCache(1, 32, 128, budget, batch=batch, q_heads=32, host_layers=1)
     q, kn, vn, s0 = bench.make_inputs(cfg, steps + warmup + 1, dev, 1, seed=7)
@@ -62,7 +62,8 @@ def point(bits, ctx, k, steps=10, warmup=3):
     avg = attn_ms / max(1, attn_n)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    out = {"bits": bits, "ctx": ctx, "topk": k, "batch": batch,
+    out = {"bits": bits, "group": group, "kernel": "fast" if cache.fast_path else "generic",
+           "ctx": ctx, "topk": k, "batch": batch,
            "k2_ms": avg, "k2_gbs": ab["hbm"] / avg / 1e6, "k2_frac_hbm": ab["hbm"] / avg / 1e6 / peaks["hbm_gbs"],
            "k2_algorithmic_bytes": ab["hbm"],
            "prefetch_bytes_per_step": pf_bytes / steps, "prefetch_ms_per_step": pf_ms / steps,
@@ -77,13 +78,16 @@ def point(bits, ctx, k, steps=10, warmup=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--group", type=int, default=32, help="quantization group size g (paper Table 4: 64)")
+    ap.add_argument("--ctx", type=int, nargs="*", help="override the context list")
+    ap.add_argument("--topk", type=int, nargs="*", help="override the top-k list")
     args = ap.parse_args()
-    ctxs = [4096, 32768, 131072] if args.quick else [4096, 16384, 65536, 131072, 262144]
-    ks = [16, 128, 512] if args.quick else [16, 64, 256, 512]
+    ctxs = args.ctx or ([4096, 32768, 131072] if args.quick else [4096, 16384, 65536, 131072, 262144])
+    ks = args.topk or ([16, 128, 512] if args.quick else [16, 64, 256, 512])
     for bits in (2, 1):
         for ctx in ctxs:
             for k in ks:
-                print(json.dumps(point(bits, ctx, k)), flush=True)
+                print(json.dumps(point(bits, ctx, k, group=args.group)), flush=True)
 
 
 if __name__ == "__main__":
