@@ -374,6 +374,12 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
     char* base = nullptr;
     rc = dalloc(c, (void**)&base, tot);
     if (rc) break;
+    // defined contents everywhere (e.g. agg beyond the frontier, which a
+    // cross-rank all-reduce of the whole buffer reads): one memset per layer
+    if (cudaMemset(base, 0, tot) != cudaSuccess) {
+      rc = fail(SPC_ECUDA, "cudaMemset of the layer buffers failed");
+      break;
+    }
     B.kcodes = (uint32_t*)(base + off[0]);
     B.vcodes = B.kcodes + G.bwords;
     B.kparams = B.kcodes + 2 * G.bwords;
