@@ -140,6 +140,16 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// shared-window addresses precomputed by the caller (the per-block issue path)
+__device__ __forceinline__ void mbar_expect_tx_u32(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_u32(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -727,10 +737,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   const uint32_t* bm_base = B.bitmap + ((size_t)b * G.U + (G.scope ? h : 0)) * (G.L / 32);
 
   // ---- TMA ring prologue -------------------------------------------------------------
-  auto issue = [&](int blk, int st) {
-    uint32_t* s = ws.stage[st];
-    mbar_expect_tx(&ws.bar[st], SL::bytes);  // the whole block record, one bulk copy
-    tma_load(s, rec_base + (size_t)blk * SL::words, SL::bytes, &ws.bar[st]);
+  // shared addresses of stage 0 / barrier 0 and their strides, computed once
+  const unsigned stage0 = smem_u32(ws.stage[0]), bar0 = smem_u32(&ws.bar[0]);
+  constexpr unsigned kStageBytes = sizeof(ws.stage[0]);
+  auto issue = [&](const uint32_t* src, int st) {
+    const unsigned bar = bar0 + 8u * st;
+    mbar_expect_tx_u32(bar, SL::bytes);  // the whole block record, one bulk copy
+    tma_load_u32(stage0 + kStageBytes * st, src, SL::bytes, bar);
   };
   if constexpr (PACK && NR == 2) {  // bk padding columns 4*NR.. are the zero rows of the PACK B fragment
     static_assert(WarpSmem<BITS, NR>::kBkRow >= 4 * NR + 4, "PACK zero padding");
@@ -743,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
 #pragma unroll
     for (int s = 0; s < kSt; ++s) {
       const int blk = blk0 + warp + s * kWarps;
-      if (blk < blk1) issue(blk, s);
+      if (blk < blk1) issue(rec_base + (size_t)blk * SL::words, s);
     }
   }
   __syncwarp();
@@ -825,10 +838,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
 
   int st = 0;
   unsigned phase = 0;
-  uint32_t bm = 0;
-  if (blk0 + warp < blk1) bm = bm_base[blk0 + warp];
-  for (int blk = blk0 + warp; blk < blk1; blk += kWarps) {
-    const uint32_t nbm = (blk + kWarps < blk1) ? bm_base[blk + kWarps] : 0u;
+  // pin bitmap words of this warp's blocks, 32 iterations per window: lane i
+  // holds block (window base + i * kWarps); the next window is loaded one
+  // window ahead, so the loop reads its word with one shuffle
+  auto bm_window = [&](int base) -> uint32_t {
+    const int bb = base + lane * kWarps;
+    return bb < blk1 ? bm_base[bb] : 0u;
+  };
+  uint32_t bm_cur = bm_window(blk0 + warp), bm_next = bm_window(blk0 + warp + 32 * kWarps);
+  // record of the block that refills the stage consumed in this iteration
+  const uint32_t* next_src = rec_base + (size_t)(blk0 + warp + kSt * kWarps) * SL::words;
+  int it = 0;
+  for (int blk = blk0 + warp; blk < blk1; blk += kWarps, ++it, next_src += kWarps * SL::words) {
+    if ((it & 31) == 0 && it) {
+      bm_cur = bm_next;
+      bm_next = bm_window(blk + 32 * kWarps);
+    }
+    const uint32_t bm = __shfl_sync(0xffffffffu, bm_cur, it & 31);
     mbar_wait(&ws.bar[st], phase);
     // order the previous block's reads of ws.sz / ws.P before this block's writes
     // by other lanes (independent thread scheduling; compute-sanitizer racecheck)
@@ -1005,12 +1031,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
         }
       }
     }
+    // this lane's tokens T = 16mt + gq + 8hf are bits 0, 8, 16, 24 of bq
+    const uint32_t bq = bm >> gq;
     if (bm) {  // pinned positions are attended from their exact rows (exact segment)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf)
-          if ((bm >> (16 * mt + gq + 8 * hf)) & 1u) {
+          if ((bq >> (16 * mt + 8 * hf)) & 1u) {
 #pragma unroll
             for (int e = 0; e < RPL; ++e) sc[mt][hf][e] = -CUDART_INF_F;
           }
@@ -1018,13 +1046,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
 #pragma unroll
     for (int e = 0; e < RPL; ++e) {
       if (spr[e]) {  // aggregate-row logits (one writer per position: pinned ones by the exact segment)
+        float* sp = spr[e] + pos0 + gq;
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            const int T = 16 * mt + gq + 8 * hf;
-            if (!((bm >> T) & 1u)) spr[e][pos0 + T] = sc[mt][hf][e];
-          }
+          for (int hf = 0; hf < 2; ++hf)
+            if (!((bq >> (16 * mt + 8 * hf)) & 1u)) sp[16 * mt + 8 * hf] = sc[mt][hf][e];
       }
     }
     float mloc[RPL];
@@ -1101,10 +1128,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
     // the stage is consumed (codes in registers, params decoded to ws.sz): refill it
     // with block it + kSt (async proxy after generic reads)
     if (lane == 0) {
-      const int nblk = blk + kSt * kWarps;
-      if (nblk < blk1) {
+      if (blk + kSt * kWarps < blk1) {
         fence_proxy_async();
-        issue(nblk, st);
+        issue(next_src, st);
       }
     }
 
@@ -1230,10 +1256,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
     __syncwarp();
     // the stage is consumed: refill it with block it + kSt (async proxy after generic reads)
     if (lane == 0) {
-      const int nblk = blk + kSt * kWarps;
-      if (nblk < blk1) {
+      if (blk + kSt * kWarps < blk1) {
         fence_proxy_async();
-        issue(nblk, st);
+        issue(next_src, st);
       }
     }
 
@@ -1267,7 +1292,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
       }
     }
     }
-    bm = nbm;
     if (++st == kSt) {
       st = 0;
       phase ^= 1u;
