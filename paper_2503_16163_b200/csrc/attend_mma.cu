@@ -206,8 +206,13 @@ struct __align__(16) WarpSmem {
   __device__ static constexpr int pidx(int row, int t) {
     return NR * 4 <= 8 ? row * 40 + t : (row & 1) * 132 + t * 4 + (row >> 1);
   }
-  float4 sz[64];                                          // value (s*2^-q, z) pairs, vparams order
+  float4 sz[64];                                          // value (s*2^-q, z) pairs, vparams order (szidx)
   uint64_t bar[kS];
+  // float4 slot f of sz, low two bits XORed with the 8-slot row index (mod 4): the
+  // decode stores (lane l -> 2l + h) and the PG loads (16 grp + 4 tq + 2 ks + h;
+  // grp = gq >> 1 for 2 rows, gq & 3 for 1 row) hit 8 distinct 16-byte bank
+  // groups per 8-lane phase (unswizzled: 2-way / 4-way conflicts)
+  __device__ static constexpr int szidx(int f) { return f ^ ((f >> 3) & 3); }
 };
 
 template <int NR>
@@ -933,8 +938,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
         o[2 * slot] = (hi - lo) * vs_lane[slot >> 1];
         o[2 * slot + 1] = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
       }
-      ws.sz[2 * lane] = make_float4(o[0], o[1], o[2], o[3]);
-      ws.sz[2 * lane + 1] = make_float4(o[4], o[5], o[6], o[7]);
+      ws.sz[WarpSmem<BITS, NR>::szidx(2 * lane)] = make_float4(o[0], o[1], o[2], o[3]);
+      ws.sz[WarpSmem<BITS, NR>::szidx(2 * lane + 1)] = make_float4(o[4], o[5], o[6], o[7]);
     }
     // key codes of this lane's tokens T0 = 16mt + gq, T1 = T0 + 8
     uint32_t kw[2][2 * BITS];
@@ -1148,8 +1153,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
         // (s', z) of tokens 16ks + 2tq + {0,1,8,9} of group grp: words 32grp + 8tq + 4ks + slot
-        const float4 sz0 = ws.sz[16 * grp + 4 * tq + 2 * ks];
-        const float4 sz1 = ws.sz[16 * grp + 4 * tq + 2 * ks + 1];
+        const float4 sz0 = ws.sz[WarpSmem<BITS, NR>::szidx(16 * grp + 4 * tq + 2 * ks)];
+        const float4 sz1 = ws.sz[WarpSmem<BITS, NR>::szidx(16 * grp + 4 * tq + 2 * ks + 1)];
         const float spr4[4] = {sz0.x, sz0.z, sz1.x, sz1.z}, zz4[4] = {sz0.y, sz0.w, sz1.y, sz1.w};
         float x[4];
         // P of tokens (t0, t0+1) and (t0+8, t0+9): two 8-byte loads
