@@ -74,6 +74,20 @@ constexpr int kMinBlocks = SPC_K2_MINB; // resident CTAs per SM
 // row) disappears from the common path.
 constexpr int kSlackLog2 = SPC_K2_LAZY ? 8 : 0;  // P <= 2^kSlackLog2
 constexpr float kSlack = (float)kSlackLog2;
+#ifndef SPC_K2_HKB
+#define SPC_K2_HKB 1
+#endif
+// f16x2 key-B build for the shared-memory query rows (NR >= 4, SPC_K2_HKB): the
+// query is split once per CTA into f16 hi + lo pairs (Qh) and the block's key
+// scales once per block into f16 hi + lo pairs (shared by all rows); per row
+// and channel pair B = Qh * sh is then formed with four f16x2 ops
+//   hi = rn(Qhi*shi),  lo = rn(Qlo*shi + rn(Qhi*slo + (Qhi*shi - hi)))
+// where Qhi*shi - hi is the exact rounding error (FMA), so hi + lo carries the
+// same ~22 bits as the fp32 product split into hi + lo (split2), at 4 instead
+// of 8 instructions per pair.  Q is pre-scaled by 2^-aq (max |Q| in [2^6, 2^7])
+// and the scales by 2^aq, so both factors stay in the f16 normal range and
+// max |B| <= 2^14 as before.
+constexpr bool kHalfKeyB = SPC_K2_HKB != 0;
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -96,6 +110,20 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
   __half2 h = *reinterpret_cast<__half2*>(&hi);
   float2 hf = __half22float2(h);
   lo = pack_f16x2(x0 - hf.x, x1 - hf.y);
+}
+
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+// (hi, lo) f16x2 of the product of two hi + lo f16x2 pairs (see kHalfKeyB)
+__device__ __forceinline__ void mul_hilo(uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl, uint32_t& hi,
+                                         uint32_t& lo) {
+  const __half2 Ah = u2h(ah), Bh = u2h(bh);
+  const __half2 H = __hmul2_rn(Ah, Bh);
+  __half2 e = __hfma2(Ah, Bh, __hneg2(H));
+  e = __hfma2(Ah, u2h(bl), e);
+  e = __hfma2(u2h(al), Bh, e);
+  hi = h2u(H);
+  lo = h2u(e);
 }
 
 __device__ __forceinline__ float fast_exp2(float x) {  // ex2.approx (|rel err| ~2^-22); -inf -> 0
@@ -250,7 +278,7 @@ struct ExactRowsSmem {
 
 template <int BITS, int NR>
 constexpr size_t fast_smem_bytes() {
-  size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps + (NR > 2 ? NR * 32 * 16 : 0), b = sizeof(MergeSmem<NR>),
+  size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps + (NR > 2 ? NR * 32 * 16 * (kHalfKeyB ? 2 : 1) : 0), b = sizeof(MergeSmem<NR>),
          c = NR == 8 ? sizeof(ExactRowsSmem<NR>) : sizeof(ExactSmem<NR>);
   return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
@@ -772,6 +800,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   constexpr bool QREG = NR <= 2;  // wide GQA rows keep the query slice in shared memory
   float Qr[QREG ? NR : 1][4];
   float4* Qs = reinterpret_cast<float4*>(smem_raw + kWarps * sizeof(WarpSmem<BITS, NR>));  // [NR][32]
+  constexpr bool HKB = kHalfKeyB && !QREG;
+  uint4* Qh = reinterpret_cast<uint4*>(Qs + NR * 32);  // [NR][32] {Qhi b0, Qhi b1, Qlo b0, Qlo b1} (HKB)
   float qabs = 0.f;
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
@@ -790,9 +820,26 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
       Qs[j * 32 + lane] = make_float4(qv[0], qv[1], qv[2], qv[3]);
     }
   }
-  if (!QREG) __syncthreads();
 #pragma unroll
   for (int o = 16; o; o >>= 1) qabs = fmaxf(qabs, __shfl_xor_sync(0xffffffffu, qabs, o));
+  const int aq = (HKB && qabs > 0.f) ? ceil_log2(qabs) - 7 : 0;  // max |Q * 2^-aq| in (2^6, 2^7]
+  if (HKB && warp == 0) {
+    const float sq = pow2i(-aq);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const float4 qq = Qs[j * 32 + lane];  // written by this lane above
+      uint4 h;
+      if (BITS == 2) {  // pairing of the key B fragment: b0 = (m0, m1), b1 = (m2, m3)
+        split2(qq.x * sq, qq.y * sq, h.x, h.z);
+        split2(qq.z * sq, qq.w * sq, h.y, h.w);
+      } else {  // b0 = (m0, m2), b1 = (m1, m3)
+        split2(qq.x * sq, qq.z * sq, h.x, h.z);
+        split2(qq.y * sq, qq.w * sq, h.y, h.w);
+      }
+      Qh[j * 32 + lane] = h;
+    }
+  }
+  if (!QREG) __syncthreads();
   const float rk = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 2 + 0]) * cs;
   const float rv = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 2 + 1]) * cs;
   const int Ek = (qabs * rk > 0.f) ? ceil_log2(qabs * rk) - 14 : 0;
@@ -800,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   // B exponent keeps kSlack bits of headroom (max|P*s'| <= 2^14 still)
   const int Ev = (rv > 0.f) ? ceil_log2(rv) - 14 + kSlackLog2 : 0;
   const int sp = BITS == 2 ? 2 * (kks & 3) : kks;       // K-index (channel) scale of this lane
-  const float kscale = cs * pow2i(-sp - Ek);              // (hi-lo) -> s * 2^(-sp-Ek)
+  const float kscale = cs * pow2i(-sp - Ek + aq);         // (hi-lo) -> s * 2^(-sp-Ek) (* 2^aq: HKB)
   const float k_out = pow2i(24 + Ek);                     // D * k_out = sum_c code * Q * s
   const float v_out = pow2i(24 + Ev);
   float vscale[4];  // value K-index (token) scales, q = 2ks + khalf
@@ -878,9 +925,29 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
         s4[m] = (hi - lo) * kscale;
         z4[m] = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
       }
+      uint32_t sh0 = 0, sl0 = 0, sh1 = 0, sl1 = 0;  // HKB: this block's scale pairs, shared by all rows
+      if (HKB) {
+        if (BITS == 2) {
+          split2(s4[0], s4[1], sh0, sl0);
+          split2(s4[2], s4[3], sh1, sl1);
+        } else {
+          split2(s4[0], s4[2], sh0, sl0);
+          split2(s4[1], s4[3], sh1, sl1);
+        }
+      }
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
         float q0, q1, q2, q3;
+        if (HKB) {
+          const float4 qq = Qs[j * 32 + lane];
+          Cp[j] = fmaf(qq.x, z4[0], fmaf(qq.y, z4[1], fmaf(qq.z, z4[2], qq.w * z4[3])));
+          const uint4 qh = Qh[j * 32 + lane];
+          uint4 frag;
+          mul_hilo(qh.x, qh.z, sh0, sl0, frag.x, frag.z);
+          mul_hilo(qh.y, qh.w, sh1, sl1, frag.y, frag.w);
+          ws.bk[kks][4 * j + (ktk ^ ((kks >> 1) & 3))] = frag;
+          continue;
+        }
         if (QREG) {
           q0 = Qr[QREG ? j : 0][0];
           q1 = Qr[QREG ? j : 0][1];
