@@ -398,15 +398,18 @@ def test_odd_topk_and_degenerate_groups(k, bits):
     cache.close()
 
 
+@pytest.mark.parametrize("bits,H,Hq", [(2, 4, 4), (1, 2, 8), (2, 2, 8)])
 @pytest.mark.parametrize("kscale,vscale,tau", [(0.01, 1000.0, 1.0), (8.0, 1e-3, 1.0), (1.0, 1.0, 30.0)])
-def test_extreme_magnitudes(kscale, vscale, tau):
+def test_extreme_magnitudes(kscale, vscale, tau, bits, H, Hq):
     """Operand-exponent paths of the fast kernel: keys scaled by 0.01 or 8,
     values by 1000 or 1e-3, and very peaky attention (query scale 30, the
-    lazy-rescale path raising its max often) -- MHA 2-bit against the oracle."""
+    lazy-rescale path raising its max often) against the oracle -- MHA 2-bit
+    and GQA-4 (8 rows per kv head: the f16x2 key-B build, whose query and
+    scale pre-scaling by 2^-aq / 2^aq must keep both factors in f16 range)."""
     import torch
     from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
     rng = np.random.default_rng(123)
-    n0, H, Hq, d, g, r, k, bits = 1200, 4, 4, 128, 32, 64, 32, 2
+    n0, d, g, r, k = 1200, 128, 32, 64, 32
     K, V = make_kv(rng, n0, H, d)
     K, V = R.bf16_round(K * kscale), R.bf16_round(V * vscale)
     st = R.LayerState(H, d, bits, g, r, k, "layer")
