@@ -21,6 +21,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "exact_segment.cuh"
 
@@ -114,7 +115,14 @@ __global__ void __launch_bounds__(256) k_agg(AttnArgs a) {
 
 void launch_agg(const AttnArgs& a, cudaStream_t st) {
   if (a.f <= 0) return;
-  const int blocks = std::min((a.f + 255) / 256, std::max(1, 2 * 148 * 4 / (a.G.U * a.G.batch)));
+  // total CTA budget of the launch (tuning: SPC_AGG_CTAS).  K3 runs on a copy
+  // stream while the next layer's K2 fills the machine; every K3 CTA takes a
+  // slot a retiring K2 CTA leaves
+  static const int budget = [] {
+    const char* e = getenv("SPC_AGG_CTAS");
+    return e ? std::max(1, atoi(e)) : 2 * 148 * 4;
+  }();
+  const int blocks = std::min((a.f + 255) / 256, std::max(1, budget / (a.G.U * a.G.batch)));
   k_agg<<<dim3(blocks, a.G.U, a.G.batch), 256, 0, st>>>(a);
 }
 

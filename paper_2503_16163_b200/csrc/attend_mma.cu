@@ -88,6 +88,13 @@ constexpr float kSlack = (float)kSlackLog2;
 // and the scales by 2^aq, so both factors stay in the f16 normal range and
 // max |B| <= 2^14 as before.
 constexpr bool kHalfKeyB = SPC_K2_HKB != 0;
+#ifndef SPC_K2_EXACT_ORDER
+#define SPC_K2_EXACT_ORDER 0
+#endif
+// CTA order of a launch: 0 = (split, head, seq) grid, each unit's exact CTA after
+// its splits; 1 = 1-D grid with every unit's splits first and all exact CTAs at
+// the end (the short exact CTAs backfill the last wave); 2 = exact CTAs first
+constexpr int kExactOrder = SPC_K2_EXACT_ORDER;
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -254,15 +261,23 @@ struct MergeSmem {
 // K and V rows is staged into shared memory with cp.async before any math
 template <int NR>
 struct ExactSmem {
-  static constexpr int CH = 128;  // (staged form: NR <= 4)
-  uint4 krow[CH][16];  // bf16 x 128 per row
+  // rows per chunk (staged form: NR <= 4).  SPC_EXACT_CH2=192 stages a whole MHA
+  // segment (64 pins + up to 95 residual + 2 in-step rows) in one chunk: faster
+  // in the one-layer harness (C2 K2 -0.4%), slower in the 32-layer bench (-0.7%,
+  // PCIe gather 47 -> 43 GB/s with the larger shared-memory footprint), so 128
+#ifndef SPC_EXACT_CH2
+#define SPC_EXACT_CH2 128
+#endif
+  static constexpr int CH = NR <= 2 ? SPC_EXACT_CH2 : 128;
+  uint4 krow[CH][16];  // bf16 x 128 per row; reused for the warps' partial outputs at the end
   uint4 vrow[CH][16];
   float sc[NR][CH];
   float fac[NR], m[NR], l[NR], pm[NR], pl[NR];
   int slots[1024];     // occupied pin slots, slot order
   int spos[1024];      // their positions
   int npin;
-  float o[kWarps][NR][128];
+  using Out = float[kWarps][NR][128];
+  __device__ Out& o() { return *reinterpret_cast<Out*>(&krow[0][0]); }
 };
 
 // exact segment scratch, direct-load form
@@ -297,6 +312,7 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
   const Geo& G = a.G;
   const LayerBufs& B = a.B;
   ExactSmem<NR>& ex = *reinterpret_cast<ExactSmem<NR>*>(smem);
+  static_assert(sizeof(typename ExactSmem<NR>::Out) <= sizeof(ex.krow), "partial outputs alias the staged key rows");
   constexpr int CH = ExactSmem<NR>::CH;
   constexpr int kRows = NR <= 2 ? 4 : 16 / NR;  // rows per warp batch
   constexpr int V = NR * kRows;                  // partial sums per lane per batch: 4, 8 or 16
@@ -472,14 +488,14 @@ __device__ void exact_segment_fast(const AttnArgs& a, const int split, const int
 #pragma unroll
   for (int j = 0; j < NR; ++j)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) ex.o[warp][j][4 * lane + i] = acc[j][i];
+    for (int i = 0; i < 4; ++i) ex.o()[warp][j][4 * lane + i] = acc[j][i];
   __syncthreads();
   const size_t base = (((size_t)b * G.H + h) * (a.nsplit + 1) + split) * NR;
   for (int i = tid; i < NR * 128; i += kThreads) {
     const int j = i >> 7, c = i & 127;
     float o = 0.f;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) o += ex.o[w][j][c];
+    for (int w = 0; w < kWarps; ++w) o += ex.o()[w][j][c];
     a.part_o[(base + j) * 128 + c] = o;
   }
   if (tid < NR) {
@@ -750,7 +766,25 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   using SL = StageLayout<BITS>;
   const Geo& G = a.G;
   const LayerBufs& B = a.B;
-  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  int split, h, b;
+  if (kExactOrder == 0) {
+    split = blockIdx.x;
+    h = blockIdx.y;
+    b = blockIdx.z;
+  } else {
+    const int units = a.G.H * a.G.batch, nmain = units * a.nsplit;
+    const int L = kExactOrder == 1 ? (int)blockIdx.x : ((int)blockIdx.x + nmain) % (nmain + units);
+    int u;
+    if (L < nmain) {
+      u = L / a.nsplit;
+      split = L - u * a.nsplit;
+    } else {
+      u = L - nmain;
+      split = a.nsplit;
+    }
+    h = u % a.G.H;
+    b = u / a.G.H;
+  }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (split == a.nsplit) {
     if constexpr (NR == 8) exact_segment_rows<NR>(a, split, h, b, smem_raw);
@@ -1468,7 +1502,8 @@ void launch_fast_t(const AttnArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(k_attend_fast<BITS, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  dim3 grid(a.nsplit + 1, a.G.H, a.G.batch);
+  dim3 grid = kExactOrder == 0 ? dim3(a.nsplit + 1, a.G.H, a.G.batch)
+                                : dim3((a.nsplit + 1) * a.G.H * a.G.batch);
   k_attend_fast<BITS, NR><<<grid, kThreads, smem, st>>>(a);
 }
 
