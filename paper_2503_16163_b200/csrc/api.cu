@@ -4,9 +4,13 @@
 // Stream structure per layer l (SURVEY.md 8(b) "Threading"):
 //   compute stream     : [wait ev_pf(l)] K2 attend (+K3 combine) -> K6a ring
 //                        append -> record ev_att(l)
-//   copy stream l % 2  : [wait ev_att(l)] K3 cross-head aggregate -> K4 top-k +
-//   (high priority)      pin diff -> K5 PCIe prefetch -> K6b slow-tier write
-//                        (+K1 migration) -> record ev_pf(l)
+//   select stream l % 2: [wait ev_att(l)] K3 cross-head aggregate -> K4 top-k +
+//   (lowest priority)    pin diff -> record ev_sel(l)
+//   copy stream l % 2  : [wait ev_sel(l)] K5 PCIe prefetch -> K6b slow-tier write
+//   (high priority)      (+K1 migration) -> record ev_pf(l)
+// The selection CTAs (a 1184-CTA aggregate, 1024-thread top-k CTAs) would
+// otherwise take every SM slot a retiring K2 CTA leaves; at low priority they
+// fill K2's gaps instead, while the PCIe gather keeps its slots.
 // Only attention sits on the caller's stream; the selection, the PCIe gather
 // and the slow-tier write for step t+1 overlap the next layers' attention.
 // decode_layer(l, t+1) waits on ev_pf(l) -- the device form of
@@ -17,6 +21,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -70,8 +75,16 @@ struct spc_cache {
   std::vector<int64_t> n, f;
   std::vector<int> ticket;  // pending ticket step per layer (-1 none)
   cudaStream_t copy_stream = nullptr, copy_stream2 = nullptr;
-  std::vector<cudaEvent_t> ev_agg, ev_pf;
+  // selection streams (K3 aggregate + K4 top-k): the copy streams themselves,
+  // or separate lower-priority streams (SPC_COPY_PRIO=split) so that the
+  // selection CTAs only take SM slots K2 leaves free while the PCIe gather keeps
+  // its high priority
+  cudaStream_t sel_stream = nullptr, sel_stream2 = nullptr;
+  std::vector<cudaEvent_t> ev_agg, ev_pf, ev_sel;
   cudaStream_t cstream(int layer) const { return (layer & 1) ? copy_stream2 : copy_stream; }
+  cudaStream_t sstream(int layer) const {
+    return sel_stream ? ((layer & 1) ? sel_stream2 : sel_stream) : cstream(layer);
+  }
   float *part_o = nullptr, *part_ml = nullptr, *pin_ml = nullptr, *spill = nullptr, *mz = nullptr;
   int32_t* staging = nullptr;
   unsigned long long* pf_rows = nullptr;
@@ -239,7 +252,7 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
   }
   CUDA_TRY(cudaEventRecord(c->ev_agg[layer], st));
   // ---- ticket + slow tier on a copy stream (transfer.py:84-94, kvcache.py:162-192) ----
-  cudaStream_t cs = c->cstream(layer);
+  cudaStream_t cs = c->sstream(layer);
   CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_agg[layer], 0));
   if (c->prof) {
     p0 = prof_event(c);
@@ -262,7 +275,12 @@ int ticket_tail(spc_cache* c, int layer, int f, int n_before, bool append_row0, 
   cudaStream_t cs = c->cstream(layer);
   cudaEvent_t p1 = nullptr;
   if (c->prof) p1 = prof_event(c);
-  launch_topk(G, c->L[layer], f, cs);
+  cudaStream_t ss = c->sstream(layer);
+  launch_topk(G, c->L[layer], f, ss);
+  if (ss != cs) {
+    CUDA_TRY(cudaEventRecord(c->ev_sel[layer], ss));
+    CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_sel[layer], 0));
+  }
   cudaEvent_t q0 = nullptr, q1 = nullptr;
   if (c->prof) {
     q0 = prof_event(c);
@@ -429,13 +447,28 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
   if (rc == SPC_OK) {
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
-    if (cudaStreamCreateWithPriority(&c->copy_stream, cudaStreamNonBlocking, hi_prio) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&c->copy_stream2, cudaStreamNonBlocking, hi_prio) != cudaSuccess)
+    // stream priorities (SPC_COPY_PRIO): "split" (default) = PCIe gather + slow-tier
+    // write on high-priority copy streams, aggregate + top-k on lowest-priority
+    // selection streams, whose CTAs then only take SM slots K2 leaves free;
+    // "high" = everything on the high-priority copy streams; "low" = everything
+    // lowest.  32-layer bench, one box: C2 999 -> 1035, C3 467 -> 531, C4 404 -> 486
+    // tok/s for high -> split
+    const char* pe = getenv("SPC_COPY_PRIO");
+    const std::string mode = pe ? pe : "split";
+    const int prio = mode == "low" ? lo_prio : hi_prio;
+    if (cudaStreamCreateWithPriority(&c->copy_stream, cudaStreamNonBlocking, prio) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->copy_stream2, cudaStreamNonBlocking, prio) != cudaSuccess)
+      rc = fail(SPC_ECUDA, "stream create failed");
+    if (rc == SPC_OK && mode == "split" &&
+        (cudaStreamCreateWithPriority(&c->sel_stream, cudaStreamNonBlocking, lo_prio) != cudaSuccess ||
+         cudaStreamCreateWithPriority(&c->sel_stream2, cudaStreamNonBlocking, lo_prio) != cudaSuccess))
       rc = fail(SPC_ECUDA, "stream create failed");
     c->ev_agg.resize(G.layers);
     c->ev_pf.resize(G.layers);
+    c->ev_sel.resize(G.layers);
     for (int l = 0; l < G.layers && rc == SPC_OK; ++l) {
       if (cudaEventCreateWithFlags(&c->ev_agg[l], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c->ev_sel[l], cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&c->ev_pf[l], cudaEventDisableTiming) != cudaSuccess)
         rc = fail(SPC_ECUDA, "event create failed");
     }
@@ -464,6 +497,9 @@ int spc_cache_destroy(spc_cache* c) {
   if (c->host_v) cudaFreeHost(c->host_v);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (auto e : c->ev_agg) if (e) cudaEventDestroy(e);
+  for (auto e : c->ev_sel) if (e) cudaEventDestroy(e);
+  if (c->sel_stream) cudaStreamDestroy(c->sel_stream);
+  if (c->sel_stream2) cudaStreamDestroy(c->sel_stream2);
   for (auto e : c->ev_pf) if (e) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->copy_stream2) cudaStreamDestroy(c->copy_stream2);
@@ -634,7 +670,7 @@ int spc_agg_buffer(spc_cache* c, int layer, float** agg, int64_t* count, void** 
   if (!c->agg_ext) return fail(SPC_EINVAL, "spc_agg_buffer needs spc_set_agg_reduce(cache, 1)");
   if (agg) *agg = c->L[layer].agg;
   if (count) *count = (int64_t)c->G.batch * c->G.U * c->G.L;
-  if (stream) *stream = (void*)c->cstream(layer);
+  if (stream) *stream = (void*)c->sstream(layer);
   return SPC_OK;
 }
 

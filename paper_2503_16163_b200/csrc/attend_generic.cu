@@ -107,7 +107,10 @@ __global__ void __launch_bounds__(256) k_agg(AttnArgs a) {
   __syncthreads();
   const float* sp = a.spill + ((size_t)b * G.Hq + h0) * G.L;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.f; i += gridDim.x * blockDim.x) {
+    // unrolled so that up to 8 heads' spill loads are in flight at once; the
+    // sum stays in ascending head order
     float acc = 0.f;
+#pragma unroll 8
     for (int x = 0; x < h1 - h0; ++x) acc += exp2f(sp[(size_t)x * G.L + i] - sM[x]) * sI[x];
     a.B.agg[((size_t)b * G.U + u) * G.L + i] = acc;
   }
