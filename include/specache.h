@@ -147,9 +147,10 @@ SPC_API int spc_debug_agg(spc_cache* cache, int layer, float* agg, void* stream)
  * aggregates must be summed before the top-k.  With spc_set_agg_reduce(c, 1),
  * spc_decode_layer / spc_predecode_layer stop after the partial aggregate; the
  * caller sums spc_agg_buffer's fp32 [batch][1][L] across ranks in place (e.g.
- * an NCCL all-reduce) on the returned copy stream, then spc_finish_layer
- * enqueues the rest of the ticket there (top-k + pin diff, PCIe prefetch,
- * slow-tier append).  Every rank then selects the same positions.  Until
+ * an NCCL all-reduce) on the returned stream (the layer's selection stream),
+ * then spc_finish_layer enqueues the rest of the ticket: top-k + pin diff on
+ * that stream, then the PCIe prefetch and slow-tier append on the layer's copy
+ * stream (ordered by an event).  Every rank then selects the same positions.  Until
  * spc_finish_layer, the next decode/predecode, spc_ticket, spc_debug_agg and
  * spc_pin of that layer return SPC_EPROTO.  kv_head scope needs no exchange
  * and no reduction. */
