@@ -3,8 +3,9 @@
 // into device memory three ways and reports GB/s:
 //   (a) zero-copy gather kernel (K5's approach: 16-byte loads through the
 //       mapped host pointer, in-flight bytes bounded by the grid);
-//   (b) cudaMemcpyBatchAsync, one descriptor per row (CUDA 12.8+);
-//   (c) one cudaMemcpyAsync per row.
+//   (b) one cudaMemcpyAsync per row.
+// (A batched-descriptor copy arm was measured in r1, profiles/r1_20_*; that
+// API is closed on this GPU pool and the arm was removed.)
 // Also the contiguous pinned H2D peak (one cudaMemcpyAsync of the same bytes).
 //
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/h2d_probe.cu -o tools/h2d_probe
@@ -85,31 +86,20 @@ static void run(size_t row_bytes, int rows, size_t slab_rows) {
   const int grids[3] = {16, 64, 296};
   for (int g = 0; g < 3; ++g)
     zc[g] = best([&] { gather<<<grids[g], 256, 0, st>>>((const uint4*)hd, (uint4*)d, dpos, rows, cpr); });
-  // (b) cudaMemcpyBatchAsync
   std::vector<void*> dsts(rows), srcs(rows);
-  std::vector<size_t> sizes(rows, row_bytes);
   for (int r = 0; r < rows; ++r) {
     dsts[r] = d + (size_t)r * row_bytes;
     srcs[r] = h + (size_t)pos[r] * row_bytes;
   }
-  cudaMemcpyAttributes attr = {};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.srcLocHint.type = cudaMemLocationTypeHost;
-  attr.dstLocHint.type = cudaMemLocationTypeDevice;
-  attr.dstLocHint.id = 0;
-  size_t attr_idx = 0, fail = 0;
-  const double batch = best([&] {
-    CK(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), rows, &attr, &attr_idx, 1, &fail, st));
-  });
-  // (c) one cudaMemcpyAsync per row
+  // (b) one cudaMemcpyAsync per row
   const double per_row = best([&] {
     for (int r = 0; r < rows; ++r)
       CK(cudaMemcpyAsync(dsts[r], srcs[r], row_bytes, cudaMemcpyHostToDevice, st));
   });
   std::printf("{\"row_bytes\": %zu, \"rows\": %d, \"MB\": %.2f, \"contiguous_peak_gbs\": %.1f, "
               "\"zero_copy_gbs\": {\"16_ctas\": %.1f, \"64_ctas\": %.1f, \"296_ctas\": %.1f}, "
-              "\"memcpy_batch_gbs\": %.1f, \"memcpy_per_row_gbs\": %.1f}\n",
-              row_bytes, rows, bytes / 1e6, peak, zc[0], zc[1], zc[2], batch, per_row);
+              "\"memcpy_per_row_gbs\": %.1f}\n",
+              row_bytes, rows, bytes / 1e6, peak, zc[0], zc[1], zc[2], per_row);
   CK(cudaFree(dpos));
   CK(cudaFree(d));
   CK(cudaFreeHost(h));
