@@ -13,15 +13,19 @@ top-k 64, one B200.  Inputs are synthetic (seeded, bf16), post-RoPE q/k/v
 (the projections around the hot path are out of scope).  Per-step data
 (~52 GB of low-bit KV) is far larger than L2 (126 MB), so no flush is needed.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c1]
   python bench.py --impl reference ...     # CPU reference arm (oracle port)
 
-Multi-GPU (torchrun, one rank per GPU): the path shards by sequence with no
-data-path collective -- every rank runs its own batch (weak scaling); NCCL is
-used only for the barrier and the max-over-ranks timing.  `--shard heads`
-instead splits the config's KV heads over the ranks (strong scaling, the
-north star's partitioning): each layer's partial top-k aggregate is summed
-across ranks by an NCCL all-reduce on the cache's copy stream (shard.py).
+Multi-GPU: one rank per GPU over NCCL.  Under torchrun the ranks come from the
+environment; `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks.  The config's GLOBAL batch is partitioned
+(shard.plan_partition, the north star's rule): by KV head first, by sequence
+where the heads run out (strong scaling, `--shard auto`, the default).  The
+ranks that share a batch slice sum each layer's partial top-k aggregate with
+an NCCL all-reduce on the cache's copy stream (engine.py:317 couples all
+heads of a sequence); nothing else crosses ranks.  `--shard replicas` runs the
+whole config on every rank (weak scaling, no collective).  `--share N` runs
+rank 0's share of an N-way partition alone on one GPU (e.g. C4's 8-GPU rank).
 """
 from __future__ import annotations
 
@@ -47,11 +51,11 @@ CONFIGS = {
                         "1-bit KV (g32, r64), top-k 128",
                layers=32, batch=8, kv_heads=8, q_heads=32, head_dim=128, ctx=131072, bits=1,
                group=32, residual=64, topk=128),
-    # BASELINE.json configs[3], one rank's share: global batch 32 over 8 GPUs -> 4
-    # sequences per rank (sequence sharding); `--gpus 8` under torchrun is C4 itself
-    "c4": dict(workload="C4: LLaMA-3-8B-shaped GQA (8 KV heads) 32-layer decode, ctx 128k, global batch 32 "
-                        "over 8 GPUs (4 per rank), 1-bit KV (g32, r64), top-k 256, full bf16 cache in pinned host",
-               layers=32, batch=4, kv_heads=8, q_heads=32, head_dim=128, ctx=131072, bits=1,
+    # BASELINE.json configs[3]: global batch 32, 8 GPUs (`--gpus 8`: one KV head per
+    # rank); `--share 8` runs one rank's share (1 KV head x 32 sequences) on one GPU
+    "c4": dict(workload="C4: LLaMA-3-8B-shaped GQA (8 KV heads) 32-layer decode, ctx 128k, global batch 32, "
+                        "1-bit KV (g32, r64), top-k 256, full bf16 cache in pinned host",
+               layers=32, batch=32, kv_heads=8, q_heads=32, head_dim=128, ctx=131072, bits=1,
                group=32, residual=64, topk=256),
     # C3's geometry at 2 bits (not a BASELINE config): the 2-bit x 8-row K2 instantiation
     "c3b2": dict(workload="C3 geometry at 2-bit: Mistral-7B-shaped GQA (8 KV heads) 32-layer decode, ctx 128k, "
@@ -63,6 +67,11 @@ CONFIGS = {
                         "top-k 64, residual 32, batch 1",
                layers=1, batch=1, kv_heads=32, q_heads=32, head_dim=128, ctx=4096, bits=2,
                group=32, residual=32, topk=64),
+    # launcher tests only (not a BASELINE config): C3's shape at 4k context, 2 layers
+    "tiny": dict(workload="tiny: C3-shaped GQA (8 KV heads), 2 layers, ctx 4096, batch 8, 1-bit KV, top-k 128 "
+                          "(launcher test config)",
+                 layers=2, batch=8, kv_heads=8, q_heads=32, head_dim=128, ctx=4096, bits=1,
+                 group=32, residual=64, topk=128),
 }
 METRIC = "decode tokens/s at 32k/128k ctx (device-timed), HBM & H2D roofline fraction"
 NEEDLES = 256        # planted high-score keys per (seq, kv head): peaky attention
@@ -232,70 +241,155 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------------------------------
-def cpu_reference_sample(cfg: dict, threads: int, units: int, seed: int = 0) -> dict:
-    """Time the CPU reference path (oracle port of engine.py:299-321: dequantize
-    every packed group, attend both rows, aggregate, select_topk) on `units`
-    (layer, seq) units of `cfg`, `threads` at a time.  Returns tokens/s
-    extrapolated to the full step (layers x batch units per `batch` tokens)."""
-    import numpy as np
-    from concurrent.futures import ThreadPoolExecutor
+def cpu_info() -> dict:
+    """Host CPU model, visible cores and numpy's BLAS thread pool."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": i.get("internal_api"), "threads": i.get("num_threads")} for i in threadpool_info()]
+    except Exception:
+        pass
+    return {"model": model, "cpus": os.cpu_count(), "blas": blas}
 
-    from oracle import restate as R
-    from oracle.synth import make_kv, make_queries, make_step_kv
 
-    H, Hq, d, n = cfg["kv_heads"], cfg["q_heads"], cfg["head_dim"], cfg["ctx"]
+class CpuSample:
+    """The CPU reference path (oracle port of engine.py:299-321: dequantize every
+    packed group, attend both rows, aggregate, select_topk) on a bounded sample
+    of `units` (layer, seq) decode units of `cfg`, prepared once (prefill
+    quantization is not part of the decode step) and timed `threads` at a time.
 
-    def prep(i):
-        rng = np.random.default_rng(seed + i)
-        st = R.LayerState(H, d, cfg["bits"], cfg["group"], cfg["residual"], cfg["topk"])
-        K, V = make_kv(rng, n, H, d)
-        st.extend(K, V)
-        st._sync_packed()  # prefill quantization is not part of the decode step
-        q = make_queries(rng, 2, Hq, d)
-        kn, vn = make_step_kv(rng, 2, H, d)
-        return st, q, kn, vn
+    One sample = one pass over the units; a full decode step is
+    layers x batch units for `batch` tokens, so the sample's tokens/s
+    equivalent is units / layers / wall."""
 
-    def run(args):
-        st, q, kn, vn = args
+    def __init__(self, cfg: dict, units: int, seed: int = 0):
+        import numpy as np
+        from concurrent.futures import ThreadPoolExecutor
+
+        from oracle import restate as R
+        from oracle.synth import make_kv, make_queries, make_step_kv
+        self.cfg, self.units = cfg, units
+        H, Hq, d, n = cfg["kv_heads"], cfg["q_heads"], cfg["head_dim"], cfg["ctx"]
+
+        def prep(i):
+            rng = np.random.default_rng(seed + i)
+            st = R.LayerState(H, d, cfg["bits"], cfg["group"], cfg["residual"], cfg["topk"])
+            K, V = make_kv(rng, n, H, d)
+            st.extend(K, V)
+            st._sync_packed()
+            q = make_queries(rng, 2, Hq, d)
+            kn, vn = make_step_kv(rng, 2, H, d)
+            return st, q, kn, vn
+
+        with ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1))) as ex:
+            self.work = list(ex.map(prep, range(units)))
+
+    def _run(self, w):
+        from oracle import restate as R
+        st, q, kn, vn = w
         t0 = time.perf_counter()
         R.decode_layer(st, q, kn, vn, append=False)
         return time.perf_counter() - t0
 
-    with ThreadPoolExecutor(max(1, min(8, threads))) as ex:
-        work = list(ex.map(prep, range(units)))
-    with ThreadPoolExecutor(threads) as ex:
-        t0 = time.perf_counter()
-        per_unit = list(ex.map(run, work))
-        wall = time.perf_counter() - t0
-    units_per_step = cfg["layers"] * cfg["batch"]
-    step_s = units_per_step * wall / units
-    return {"value": cfg["batch"] / step_s, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": f"{units} of {units_per_step} (layer, seq) decode units of {cfg['workload'][:2]} "
-                      f"(n={n}), {threads} threads, wall {wall:.2f}s, "
-                      f"median unit {sorted(per_unit)[len(per_unit) // 2]:.2f}s; "
-                      f"tokens/s extrapolated to the full step"}
+    def time(self, threads: int) -> dict:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(threads) as ex:
+            t0 = time.perf_counter()
+            per_unit = list(ex.map(self._run, self.work))
+            wall = time.perf_counter() - t0
+        return {"wall_s": wall, "median_unit_s": sorted(per_unit)[len(per_unit) // 2],
+                "tokens_per_s": self.units / self.cfg["layers"] / wall}
+
+    def single_core(self) -> dict:
+        """One unit on one thread with the BLAS pool limited to 1."""
+        try:
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                s = self._run(self.work[0])
+        except ImportError:
+            s = self._run(self.work[0])
+        return {"unit_s": s, "tokens_per_s": 1.0 / self.cfg["layers"] / s}
+
+
+def cpu_reference_sample(cfg: dict, threads: int, units: int, seed: int = 0, single: bool = True) -> dict:
+    """cpu_baseline for the GPU arm: one timed sample (see CpuSample)."""
+    smp = CpuSample(cfg, units, seed)
+    r = smp.time(threads)
+    one = smp.single_core() if single else None
+    full = cfg["layers"] * cfg["batch"]
+    return {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{units} of {full} (layer, seq) decode units of {cfg['workload'][:2]} (n={cfg['ctx']}), "
+                      f"{threads} threads, wall {r['wall_s']:.2f}s, median unit {r['median_unit_s']:.2f}s; "
+                      f"tokens/s = units / layers / wall",
+            "single_core": one, "cpu": cpu_info(),
+            "note": "oracle/restate.py: vectorised numpy restatement of the reference's per-layer decode "
+                    "(the reference itself is pure Python and does not travel to the GPU box; its own "
+                    "timing in the build container is profiles/r2_reference_c1_timing.json)"}
+
+
+def workload_config(cfg: dict, world: int, args, part=None) -> dict:
+    """The `config` object both arms print (same workload, same keys)."""
+    d, B, g = cfg["head_dim"], cfg["bits"], cfg["group"]
+    kv_gb = cfg["layers"] * cfg["batch"] * cfg["kv_heads"] * cfg["ctx"] * d * (B / 4 + 8 / g) / 1e9
+    if args.shard == "replicas":
+        par = f"replicas x{world}: the whole config on every rank (no collective)"
+        gb = cfg["batch"] * world
+    else:
+        if part is None:
+            from paper_2503_16163_b200.shard import plan_partition
+            part = plan_partition(cfg["kv_heads"], cfg["q_heads"], cfg["batch"], 0, max(world, args.share or 1),
+                                  args.shard)
+        par = part.describe()
+        if part.head_groups > 1:
+            par += "; per-layer NCCL all-reduce of the top-k aggregate over each batch slice's ranks"
+        if args.share and world == 1 and args.share > 1:
+            par = f"rank 0 of {args.share} alone on 1 GPU: " + par
+        gb = cfg["batch"]
+    return {"workload": cfg["workload"], "global_batch": gb, "seq_len": cfg["ctx"], "layers": cfg["layers"],
+            "bits": cfg["bits"], "group": g, "residual": cfg["residual"], "topk": cfg["topk"],
+            "kv_heads": cfg["kv_heads"], "q_heads": cfg["q_heads"], "head_dim": d, "parallelism": par,
+            "l2": "no flush: per-step low-bit KV %.1f GB >> 126 MB L2" % kv_gb}
 
 
 def run_reference_arm(args, cfg):
+    """`--impl reference`: the CPU reference path (oracle port) on this box's
+    host cores, rank 0 only.  Each step is one bounded sample (CpuSample) of
+    the workload; ms_per_step is that sample's real wall time and value its
+    tokens/s equivalent, so `steps x ms_per_step` is the time actually spent."""
     rank, world, _, _ = dist_env()
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    units = threads
+    units = max(1, min(threads, 16))
+    smp = CpuSample(cfg, units)
     vals = []
     for i in range(args.warmup + args.steps):
-        r = cpu_reference_sample(cfg, threads, units, seed=1000 * i)
+        r = smp.time(threads)
         if i >= args.warmup:
             vals.append(r)
-    value = sum(v["value"] for v in vals) / len(vals)
-    base = vals[-1]
-    base["value"] = value
+    one = smp.single_core()
+    wall = sum(v["wall_s"] for v in vals)
+    value = units * len(vals) / cfg["layers"] / wall
+    full = cfg["layers"] * cfg["batch"]
+    base = {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"each step: {units} of {full} (layer, seq) decode units of {cfg['workload'][:2]} "
+                      f"(n={cfg['ctx']}) on {threads} threads; tokens/s = units / layers / wall",
+            "units_per_step": units, "full_step_units": full, "timed_wall_s": wall,
+            "single_core": one, "cpu": cpu_info()}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * cfg["batch"] / value, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "global_batch": cfg["batch"], "seq_len": cfg["ctx"],
-                       "parallelism": "cpu threads"},
+            "ms_per_step": 1000.0 * wall / len(vals), "higher_is_better": True,
+            "scaling": "weak" if args.shard == "replicas" else "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded)", "config": workload_config(cfg, args.gpus, args),
             "cpu_baseline": base,
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -350,7 +444,7 @@ def prefill_cache(cache, cfg, host_layers, s0, device, seed):
         torch.cuda.synchronize(device)
 
 
-def agg_reducer(cache, layers, device):
+def agg_reducer(cache, layers, device, group=None):
     """Per-layer cross-rank sum of the partial top-k aggregate for a KV-head
     sharded cache (shard.py): NCCL all-reduce on the layer's copy stream, then
     the rest of the ticket (spc_finish_layer).  Views and streams are built once."""
@@ -371,7 +465,7 @@ def agg_reducer(cache, layers, device):
     def reduce(layer):
         v, s = views[layer]
         with torch.cuda.stream(s):
-            dist.all_reduce(v)
+            dist.all_reduce(v, group=group)
         _lib.check(lib.spc_finish_layer(h, layer))
 
     return reduce
@@ -386,22 +480,13 @@ def run_gpu_arm(args, cfg):
     from paper_2503_16163_b200 import _lib
 
     rank, world, local, local_world = dist_env()
-    torch.cuda.set_device(local)
-    device = f"cuda:{local}"
-    heads = args.shard == "heads"
-    if world > 1 or heads:  # head sharding reduces the aggregate even at N=1 (a 1-rank NCCL group)
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
-        dist.init_process_group("nccl", device_id=torch.device(device), rank=rank, world_size=world)
-    if heads:
-        from paper_2503_16163_b200.shard import head_shard
-        sh = head_shard(cfg["kv_heads"], cfg["q_heads"], rank, world)
-        cfg = dict(cfg, kv_heads=sh.kv_heads, q_heads=sh.q_heads)
+    device, group, part, lcfg, reduce_agg = setup_ranks(args, cfg)
 
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        cpu_base = cpu_reference_sample(cfg, threads, threads)
+        cpu_base = cpu_reference_sample(cfg, threads, max(1, min(threads, 16)))
+    gcfg, cfg = cfg, lcfg   # gcfg: the global workload; cfg: this rank's share
 
     W, K = args.warmup, args.steps
     total_steps = 2 * (W + K)  # device-timed pass + end-to-end pass
@@ -410,13 +495,13 @@ def run_gpu_arm(args, cfg):
                          prefetch_k=cfg["topk"], context_length=cfg["ctx"] + total_steps + 64)
     t_setup = time.perf_counter()
     cache = DeviceTwoTierCache(cfg["layers"], cfg["kv_heads"], cfg["head_dim"], budget,
-                               batch=cfg["batch"], q_heads=cfg["q_heads"], device=local,
+                               batch=cfg["batch"], q_heads=cfg["q_heads"], device=torch.device(device).index,
                                host_layers=host_layers)
     reduce_layer = None
-    if heads:
+    if reduce_agg:
         from paper_2503_16163_b200.shard import allreduce_sum
-        dec = SpeculativeLayerDecoder(cache, agg_reduce=allreduce_sum())
-        reduce_layer = agg_reducer(cache, cfg["layers"], device)
+        dec = SpeculativeLayerDecoder(cache, agg_reduce=allreduce_sum(group))
+        reduce_layer = agg_reducer(cache, cfg["layers"], device, group)
     else:
         dec = SpeculativeLayerDecoder(cache)
     q, k_new, v_new, s0 = make_inputs(cfg, total_steps + 1, device, host_layers, seed=1234 + rank)
@@ -466,7 +551,7 @@ def run_gpu_arm(args, cfg):
     torch.cuda.synchronize(device)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     newpins = []
-    with ClockSampler(local) as clocks:
+    with ClockSampler(torch.device(device).index) as clocks:
         ev0.record()
         for _ in range(K):
             step_device(t, q[t], k_new[t], v_new[t])
@@ -546,7 +631,9 @@ def run_gpu_arm(args, cfg):
     d2h = o_h.numel() * 2 + pm_h.numel() * 4
 
     ms_per_step = elapsed_ms / K
-    tokens = cfg["batch"] * K if heads else whole_job_tokens(cfg["batch"], K, world)
+    # strong partition: the ranks together decode the global batch per step;
+    # replicas: every rank its own copy of the config (weak scaling)
+    tokens = whole_job_tokens(gcfg["batch"], K, world) if args.shard == "replicas" else gcfg["batch"] * K
     value = tokens / (elapsed_ms / 1e3)
     ab = algorithmic_bytes_per_layer(cfg, n_mid + K // 2, f_mid, npin)
     attn_avg_ms = attn_ms / max(1, attn_n)
@@ -570,17 +657,14 @@ def run_gpu_arm(args, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if heads else "weak",
+        "scaling": "weak" if args.shard == "replicas" else "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; peaky: %d needle keys per "
         "(seq, kv head), q drift sigma %.1f)" % (NEEDLES, DRIFT),
-        "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * (1 if heads else world),
-                   "seq_len": cfg["ctx"], "layers": cfg["layers"],
-                   "parallelism": (f"kv-heads x{world} ({cfg['kv_heads']} kv / {cfg['q_heads']} q heads per rank; "
-                                   "per-layer NCCL all-reduce of the top-k aggregate on the copy stream)") if heads
-                   else f"replicas-by-sequence x{world} (no collective)",
-                   "bits": cfg["bits"], "topk": cfg["topk"], "l2": "no flush: per-step KV traffic "
-                   "%.1f GB >> 126 MB L2" % (ab["hbm"] * cfg["layers"] / 1e9),
-                   "host_layers": host_layers, "attention_impl": "fast" if cache.fast_path else "generic"},
+        "config": workload_config(gcfg, world, args, part),
+        "rank_share": {"kv_heads": cfg["kv_heads"], "q_heads": cfg["q_heads"], "batch": cfg["batch"],
+                       "host_layers": host_layers, "attention_impl": "fast" if cache.fast_path else "generic",
+                       "host_slabs_note": "layers l, l' with l = l' mod host_layers share one pinned slow-tier "
+                                          "slab and are fed identical KV (host RAM); PCIe bytes unchanged"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": "K2 attend (per layer launch, all sequences)",
@@ -610,6 +694,59 @@ def run_gpu_arm(args, cfg):
     if dist.is_initialized():
         dist.destroy_process_group()
     return 0
+
+
+def setup_ranks(args, cfg):
+    """Device, process group and this rank's share of the partition.
+
+    Returns (device, agg_group, partition, rank_cfg, reduce_agg).  NCCL by
+    default (SPC_BENCH_BACKEND=gloo for two ranks sharing one GPU in tests);
+    rank r uses GPU LOCAL_RANK mod the visible device count."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_16163_b200.shard import plan_partition
+    rank, world, local, _ = dist_env()
+    ndev = max(1, torch.cuda.device_count())
+    dev_index = local % ndev
+    torch.cuda.set_device(dev_index)
+    device = f"cuda:{dev_index}"
+    part, lcfg, group, reduce_agg = None, dict(cfg), None, False
+    if args.shard != "replicas":
+        share = args.share if (world == 1 and args.share) else world
+        part = plan_partition(cfg["kv_heads"], cfg["q_heads"], cfg["batch"], rank if world > 1 else 0, share,
+                              args.shard)
+        lcfg = dict(cfg, kv_heads=part.heads.kv_heads, q_heads=part.heads.q_heads, batch=part.batch)
+        # the agg all-reduce: across the head groups of a batch slice; `--shard heads`
+        # at N=1 exercises it as a 1-rank group
+        reduce_agg = (world > 1 and part.head_groups > 1) or (world == 1 and args.shard == "heads" and share == 1)
+    if world > 1 or reduce_agg:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+        backend = os.environ.get("SPC_BENCH_BACKEND", "nccl")
+        kw = {"device_id": torch.device(device)} if backend == "nccl" else {}
+        dist.init_process_group(backend, rank=rank, world_size=world, **kw)
+        if reduce_agg and part is not None and part.batch_groups > 1:
+            for ranks in part.all_agg_groups():   # every rank creates every group, in order
+                g = dist.new_group(ranks)
+                if rank in ranks:
+                    group = g
+    return device, group, part, lcfg, reduce_agg
+
+
+def relaunch_under_torchrun(argv, nproc: int) -> int:
+    """`--gpus N` outside torchrun: re-run this script with N ranks
+    (torch.distributed.run, 127.0.0.1 rendezvous); rank 0's JSON line passes
+    through on stdout."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+    print(f"[bench] relaunching under torchrun: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
 
 
 # model shapes around the hot path for --full-decoder (hidden, ffn, vocab); random-init weights
@@ -643,7 +780,7 @@ def run_full_decoder(args, cfg):
     rank, world, local, local_world = dist_env()
     torch.cuda.set_device(local)
     device = f"cuda:{local}"
-    heads = args.shard == "heads"
+    heads = args.shard == "heads" or (args.shard == "auto" and world > 1)
     if world > 1 or heads:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
@@ -735,6 +872,32 @@ def run_full_decoder(args, cfg):
     return 0
 
 
+def run_dry(args, cfg):
+    """The launcher and partition logic on CPU (gloo): every rank reports its
+    share; rank 0 prints one JSON line with the partition."""
+    import torch.distributed as dist
+
+    from paper_2503_16163_b200.shard import plan_partition
+    rank, world, _, _ = dist_env()
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    part = plan_partition(cfg["kv_heads"], cfg["q_heads"], cfg["batch"], rank, world,
+                          "seq" if args.shard == "replicas" else args.shard)
+    mine = {"rank": rank, "kv": [part.heads.kv_lo, part.heads.kv_hi], "q": [part.heads.q_lo, part.heads.q_hi],
+            "seqs": [part.seq_lo, part.seq_hi], "agg_group": part.agg_group}
+    shares = [None] * world
+    if world > 1:
+        dist.all_gather_object(shares, mine)
+        dist.destroy_process_group()
+    else:
+        shares = [mine]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "config": workload_config(cfg, world, args, part),
+                          "ranks": shares}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -744,17 +907,26 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--host-layers", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--shard", default="seq", choices=["seq", "heads"],
-                    help="multi-GPU partition: by sequence (no collective; default) or by KV head "
-                         "(layer-scope top-k: per-layer NCCL all-reduce of the aggregate on the copy stream)")
+    ap.add_argument("--shard", default="auto", choices=["auto", "heads", "seq", "replicas"],
+                    help="multi-GPU partition of the global batch: auto = by KV head, then by sequence "
+                         "where heads run out (default, the north star's rule); heads; seq; or replicas "
+                         "(whole config on every rank, weak scaling)")
+    ap.add_argument("--share", type=int, default=0,
+                    help="run rank 0's share of an N-way partition alone on one GPU")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without a GPU: init the process group (gloo), print the partition")
     ap.add_argument("--full-decoder", action="store_true",
                     help="time the whole model step around the hot path (SURVEY 8(f) row 1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = dict(CONFIGS[args.config])
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        return relaunch_under_torchrun(sys.argv[1:], args.gpus)
     if args.impl == "reference":
         return run_reference_arm(args, cfg)
+    if args.dry_run:
+        return run_dry(args, cfg)
     if args.full_decoder:
         return run_full_decoder(args, cfg)
     return run_gpu_arm(args, cfg)

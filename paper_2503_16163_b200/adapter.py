@@ -53,7 +53,9 @@ class DeviceSpeculativeDecoder(ToyModel):
 
     def __init__(self, config, weights, budget: CacheBudget, channel_model: ChannelModel | None = None,
                  mode: str = "sim", compute_time_per_step: float = 0.0, prefill_time: float = 0.0,
-                 device: int = 0, clock: str = "logical"):
+                 device: int = 0, clock: str = "logical", capacity: int | None = None):
+        import dataclasses
+
         import torch
         if mode not in ("sim", "thread"):
             raise ValueError("mode must be 'sim' or 'thread'")
@@ -64,7 +66,14 @@ class DeviceSpeculativeDecoder(ToyModel):
         self._ev = None
         ToyModel.__init__(self, config, weights, device)
         self.budget = budget
-        self.cache = DeviceTwoTierCache(config.layers, config.kv_heads, config.head_dim, budget,
+        # The reference decodes past context_length and max_len (context_length
+        # only feeds memory_ratio, kvcache.py:55-63; decode_step has no length
+        # check, engine.py:286-339).  The device cache is sized by `capacity`
+        # (default: max(context_length, max_len) + 1024 positions); self.budget
+        # keeps the caller's budget.
+        cap = capacity if capacity is not None else max(budget.context_length, config.max_len) + 1024
+        dev_budget = dataclasses.replace(budget, context_length=max(cap, budget.context_length))
+        self.cache = DeviceTwoTierCache(config.layers, config.kv_heads, config.head_dim, dev_budget,
                                         q_heads=config.q_heads, device=device)
         self.layer_dec = SpeculativeLayerDecoder(self.cache)
         self.channel_model = channel_model or ChannelModel()
@@ -238,8 +247,10 @@ def generate(config, weights, prompt, steps: int, budget: CacheBudget,
     """engine.py:342-386 on the device (clock: see the module docstring)."""
     if steps < 1:
         raise ValueError("steps must be >= 1")
+    prompt = list(prompt)
     dec = DeviceSpeculativeDecoder(config, weights, budget, channel_model, mode,
-                                   compute_time_per_step, prefill_time, device, clock)
+                                   compute_time_per_step, prefill_time, device, clock,
+                                   capacity=max(budget.context_length, len(prompt) + steps + 2))
     try:
         tokens = [dec.prefill(prompt)]
         dec.predecode()

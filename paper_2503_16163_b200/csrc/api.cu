@@ -702,6 +702,7 @@ int spc_debug_agg(spc_cache* c, int layer, float* agg, void* stream) {
   if (int rc = check_layer(c, layer)) return rc;
   if (int rc = check_not_pending(c, layer)) return rc;
   const Geo& G = c->G;
+  CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));
   CUDA_TRY(cudaMemcpyAsync(agg, c->L[layer].agg, (size_t)G.batch * G.U * G.L * 4, cudaMemcpyDeviceToDevice, st));
@@ -711,6 +712,8 @@ int spc_debug_agg(spc_cache* c, int layer, float* agg, void* stream) {
 int spc_materialize(spc_cache* c, int layer, int seq, int head, float* keys, float* values, void* stream) {
   if (int rc = check_layer(c, layer)) return rc;
   if (seq < 0 || seq >= c->G.batch || head < 0 || head >= c->G.H) return fail(SPC_EINVAL, "seq/head out of range");
+  if (int rc = check_not_pending(c, layer)) return rc;
+  CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[layer], 0));
   launch_materialize(c->G, c->L[layer], seq, head, (int)c->n[layer], (int)c->f[layer], keys, values, st);
@@ -723,6 +726,11 @@ int spc_export_packed(spc_cache* c, int layer, int seq, uint8_t* kc, uint16_t* k
   if (int rc = check_layer(c, layer)) return rc;
   if (c->G.bits == 16) return fail(SPC_EINVAL, "16-bit tier has no packed groups");
   if (seq < 0 || seq >= c->G.batch) return fail(SPC_EINVAL, "seq out of range");
+  if (int rc = check_not_pending(c, layer)) return rc;
+  CUDA_TRY(cudaSetDevice(c->device));
+  // the newest group's migration (K1) runs on the layer's copy stream after the
+  // host frontier has advanced: wait for it like spc_materialize does
+  CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_pf[layer], 0));
   launch_export(c->G, c->L[layer], seq, (int)(c->f[layer] / c->G.g), kc, kz, ks, vc, vz, vs,
                 (cudaStream_t)stream);
   CUDA_TRY(cudaGetLastError());

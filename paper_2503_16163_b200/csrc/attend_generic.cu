@@ -35,11 +35,7 @@ __global__ void __launch_bounds__(kCH) k_attend_generic(AttnArgs a) {
 void launch_attend_generic(const AttnArgs& a, cudaStream_t st) {
   const Geo& G = a.G;
   size_t smem = generic_smem_bytes(G, a.rows);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_attend_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
+  cudaFuncSetAttribute(k_attend_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);  // per device
   dim3 grid(a.nsplit + 1, G.H, G.batch);
   k_attend_generic<<<grid, kCH, smem, st>>>(a);
 }

@@ -1497,11 +1497,7 @@ void launch_fast_t(const AttnArgs& a, cudaStream_t st) {
   constexpr size_t smem = fast_smem_bytes<BITS, NR>();
   // two CTAs per SM (228 KB, 1 KB reserved per CTA) is the design point
   static_assert(smem * kMinBlocks <= 227 * 1024, "K2 shared memory exceeds kMinBlocks CTAs/SM");
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_attend_fast<BITS, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  cudaFuncSetAttribute(k_attend_fast<BITS, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  // per device
   dim3 grid = kExactOrder == 0 ? dim3(a.nsplit + 1, a.G.H, a.G.batch)
                                 : dim3((a.nsplit + 1) * a.G.H * a.G.batch);
   k_attend_fast<BITS, NR><<<grid, kThreads, smem, st>>>(a);

@@ -26,7 +26,8 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
   float* sv = sk + g * d;                                    // [g][d]
   uint32_t* wk = reinterpret_cast<uint32_t*>(sv + g * d);    // [R][tb*krw]
   uint32_t* wv = wk + nw;                                    // [R][tb*vrw]
-  double* kz = reinterpret_cast<double*>(wv + nw + (nw & 1));  // [d]
+  // float64 params start at the next 8-byte boundary after the code words
+  double* kz = reinterpret_cast<double*>(smem_raw + ((sizeof(float) * 2 * g * d + sizeof(uint32_t) * 2 * nw + 7) & ~size_t(7)));  // [d]
   double* ks = kz + d;
   double* vz = ks + d;                                       // [g][nch]
   double* vs = vz + g * G.nch;
@@ -314,7 +315,8 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
 
 size_t quantize_smem_bytes(const Geo& G) {
   size_t s = 2 * sizeof(float) * G.g * G.d;
-  s += sizeof(uint32_t) * (2 * (G.g / G.tb) * G.bwords + 2);
+  s += sizeof(uint32_t) * (2 * (G.g / G.tb) * G.bwords);
+  s = (s + 7) & ~size_t(7);
   s += sizeof(double) * (2 * G.d + 2 * G.g * G.nch);
   return s;
 }
@@ -322,11 +324,9 @@ size_t quantize_smem_bytes(const Geo& G) {
 void launch_quantize(const Geo& G, const LayerBufs& B, const QuantSrc& S, int blk0, int nblocks,
                      cudaStream_t st) {
   if (nblocks <= 0) return;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_quantize, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
+  // set on every launch: the attribute is per device, and a process-wide flag
+  // would skip the second device of a multi-device process
+  cudaFuncSetAttribute(k_quantize, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   dim3 grid(nblocks, G.H, G.batch);
   if (G.fast && G.d == 128 && G.g == 32 && (G.bits == 1 || G.bits == 2)) {
     if (G.bits == 2) k_quantize_fast<2><<<grid, 256, 0, st>>>(G, B, S, blk0);

@@ -165,7 +165,9 @@ def select_topk(scores, k: int, eligible=None, device: int = 0) -> tuple:
     """Device select_topk (engine.py:75-84) for eligible = range(n) (the
     packed-positions domain): k highest, ties to the lower position, sorted."""
     import torch
-    s = torch.as_tensor(np.asarray(scores, np.float32), device=f"cuda:{device}")
+    # + 0.0 turns -0.0 into +0.0: the radix select orders raw fp32 bit patterns,
+    # and the reference treats -0.0 == 0.0 (stable argsort, engine.py:82)
+    s = torch.as_tensor(np.asarray(scores, np.float32), device=f"cuda:{device}") + 0.0
     n = s.numel() if eligible is None else len(eligible)
     if eligible is not None and list(eligible) != list(range(n)):
         raise ValueError("device select_topk supports eligible = range(n)")
@@ -174,6 +176,7 @@ def select_topk(scores, k: int, eligible=None, device: int = 0) -> tuple:
     if bool((s[:n] < 0).any()):
         raise ValueError("device select_topk expects non-negative scores (probability mass)")
     out = torch.empty(k, dtype=torch.int32, device=s.device)
-    _lib.check(_lib.lib().spc_select_topk(s.data_ptr(), n, k, out.data_ptr(),
-                                          current_stream(s.device)))
+    with torch.cuda.device(s.device):
+        _lib.check(_lib.lib().spc_select_topk(s.data_ptr(), n, k, out.data_ptr(),
+                                              current_stream(s.device)))
     return tuple(int(p) for p in out.cpu().tolist() if p >= 0)

@@ -27,9 +27,10 @@ aggregate values are that close (SURVEY 8(c) parity contract (2)).
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
-__all__ = ["HeadShard", "head_shard", "allreduce_sum"]
+__all__ = ["HeadShard", "head_shard", "allreduce_sum", "Partition", "plan_partition"]
 
 
 @dataclass(frozen=True)
@@ -83,3 +84,69 @@ def allreduce_sum(group=None):
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 
     return reduce
+
+
+@dataclass(frozen=True)
+class Partition:
+    """One rank's share of a (KV head x sequence) partition of a box.
+
+    The world is laid out as ``head_groups`` x ``batch_groups``: rank r owns
+    the head shard ``r % head_groups`` of the sequences in batch slice
+    ``r // head_groups``.  The ranks of one batch slice together hold every
+    head of those sequences, so the layer-scope aggregate (engine.py:317) is
+    reduced over ``agg_group`` only; batch slices never exchange data."""
+    rank: int
+    world: int
+    head_groups: int
+    batch_groups: int
+    heads: HeadShard
+    seq_lo: int
+    seq_hi: int
+
+    @property
+    def batch(self) -> int:
+        return self.seq_hi - self.seq_lo
+
+    @property
+    def agg_group(self) -> list:
+        """Ranks that share this rank's sequences (the agg all-reduce group)."""
+        b = self.rank // self.head_groups
+        return [b * self.head_groups + h for h in range(self.head_groups)]
+
+    def all_agg_groups(self) -> list:
+        return [[b * self.head_groups + h for h in range(self.head_groups)] for b in range(self.batch_groups)]
+
+    def describe(self) -> str:
+        return (f"kv-heads x{self.head_groups} * sequences x{self.batch_groups} "
+                f"({self.heads.kv_heads} kv / {self.heads.q_heads} q heads, {self.batch} seqs per rank)")
+
+
+def plan_partition(kv_heads: int, q_heads: int, batch: int, rank: int, world: int,
+                   mode: str = "auto") -> Partition:
+    """The north star's partitioning of one box: by KV head
+    first, by sequence where heads run out.
+
+    mode "auto"  : head_groups = gcd(world, kv_heads), batch_groups = the rest;
+    mode "heads" : all ranks split the heads (kv_heads % world == 0);
+    mode "seq"   : all ranks split the sequences (no collective at all).
+    Raises ValueError when the batch does not split over the batch groups."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError("rank must be in [0, world)")
+    if mode == "auto":
+        hg = math.gcd(world, kv_heads)
+    elif mode == "heads":
+        hg = world
+    elif mode == "seq":
+        hg = 1
+    else:
+        raise ValueError("mode must be 'auto', 'heads' or 'seq'")
+    if kv_heads % hg:
+        raise ValueError(f"kv_heads={kv_heads} does not split over {hg} head groups")
+    bg = world // hg
+    if bg * hg != world or batch % bg:
+        raise ValueError(f"batch={batch} does not split over {bg} sequence groups "
+                         f"({world} ranks, {hg} head groups)")
+    hs = head_shard(kv_heads, q_heads, rank % hg, hg)
+    per = batch // bg
+    b = rank // hg
+    return Partition(rank, world, hg, bg, hs, b * per, (b + 1) * per)

@@ -170,3 +170,59 @@ def test_head_shard_ranges():
         head_shard(8, 32, 0, 3)      # heads run out -> shard by sequence instead
     with pytest.raises(ValueError):
         head_shard(8, 32, 4, 4)
+
+
+# ---- the bench launcher and the (KV head x sequence) partition (bench.py --gpus N) ----
+def test_plan_partition_heads_then_batch():
+    from paper_2503_16163_b200.shard import plan_partition
+    # C3: 8 KV heads over 2/4/8 ranks -> pure head sharding, global batch 8 on every rank
+    for n in (2, 4, 8):
+        parts = [plan_partition(8, 32, 8, r, n) for r in range(n)]
+        assert all(p.head_groups == n and p.batch_groups == 1 and p.batch == 8 for p in parts)
+        assert sorted((p.heads.kv_lo, p.heads.kv_hi) for p in parts) == [(i * 8 // n, (i + 1) * 8 // n)
+                                                                       for i in range(n)]
+        assert all(p.agg_group == list(range(n)) for p in parts)
+    # heads run out: 16 ranks over 8 KV heads -> 2 batch slices of 16 sequences (C4's batch 32)
+    parts = [plan_partition(8, 32, 32, r, 16) for r in range(16)]
+    assert {(p.head_groups, p.batch_groups) for p in parts} == {(8, 2)}
+    assert parts[3].seq_lo == 0 and parts[11].seq_lo == 16 and parts[11].heads.kv_lo == 3
+    assert parts[11].agg_group == list(range(8, 16))
+    # 3 ranks, 8 heads: gcd 1 -> batch sharding; C3's batch 8 does not split over 3
+    with pytest.raises(ValueError):
+        plan_partition(8, 32, 8, 0, 3)
+    assert plan_partition(8, 32, 6, 2, 3).seq_lo == 4
+    assert plan_partition(32, 32, 16, 1, 2, "seq").heads.kv_heads == 32
+
+
+def _dry(args):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args, capture_output=True, text=True,
+                         timeout=240, cwd="/tmp", env=dict(os.environ, PYTHONPATH=root))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+@pytest.mark.timeout(300)
+def test_bench_gpus_flag_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun relaunches itself with 2 ranks
+    (torch.distributed.run); rank 0 alone prints the JSON line."""
+    d = _dry(["--gpus", "2", "--config", "c3", "--dry-run"])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 8
+    assert [r["kv"] for r in d["ranks"]] == [[0, 4], [4, 8]]
+    assert all(r["seqs"] == [0, 8] and r["agg_group"] == [0, 1] for r in d["ranks"])
+
+
+@pytest.mark.timeout(300)
+def test_reference_arm_config_matches_gpu_arm():
+    """Both arms print the same `config` object for the same workload."""
+    import argparse
+    import bench
+    args = argparse.Namespace(shard="auto", share=0, gpus=2)
+    a = bench.workload_config(dict(bench.CONFIGS["c3"]), 2, args)
+    d = _dry(["--gpus", "2", "--config", "c3", "--dry-run"])
+    assert a == d["config"]
