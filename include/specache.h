@@ -139,6 +139,19 @@ SPC_API int spc_ticket(spc_cache* cache, int layer, int32_t* picked, int32_t* ne
 SPC_API int spc_select_topk(const float* scores, int n, int k, int32_t* out, void* stream);
 /* Debug: speculative-row aggregate of `layer`, device fp32 [batch][units][context_length]. */
 SPC_API int spc_debug_agg(spc_cache* cache, int layer, float* agg, void* stream);
+/* Debug (parity tests): when enabled, every decode / predecode layer also keeps its
+ * attention output in fp32 before the bf16 rounding (the north star's tolerance
+ * applies to the fp32-accumulated result; bf16 I/O adds one RN rounding). */
+SPC_API int spc_debug_output_f32(spc_cache* cache, int enable);
+/* Wall time (ms) of the K5 prefetch kernels of the last profiled window: the
+ * union of their intervals on the two copy streams. */
+SPC_API double spc_profile_prefetch_wall_ms(const spc_cache* cache);
+/* Host-link roofline: best of 5 pinned host -> device transfers of `bytes`, by
+ * DMA (cudaMemcpyAsync) and by a zero-copy read kernel (K5's mechanism), GB/s. */
+SPC_API int spc_h2d_peak(int device, int64_t bytes, double* dma_gbs, double* zero_copy_gbs);
+/* The last fp32 output of `layer`: device fp32 [batch][rows][q_heads][head_dim]
+ * (rows = 1 after predecode, 2 after decode; room for 2 rows is copied). */
+SPC_API int spc_debug_out_f32(spc_cache* cache, int layer, float* out, void* stream);
 
 /* -- KV-head sharding with layer-scope top-k (collective (2)) -----
  * A rank that owns kv heads [h0, h1) of every sequence builds its cache with

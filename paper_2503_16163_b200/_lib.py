@@ -49,6 +49,10 @@ _SIGS = {
     "spc_decode_layer": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P]),
     "spc_ticket": (_I, [_P, _I, _P, _P, _P]),
     "spc_debug_agg": (_I, [_P, _I, _P, _P]),
+    "spc_debug_output_f32": (_I, [_P, _I]),
+    "spc_profile_prefetch_wall_ms": (ctypes.c_double, [_P]),
+    "spc_h2d_peak": (_I, [_I, _I64, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "spc_debug_out_f32": (_I, [_P, _I, _P, _P]),
     "spc_set_agg_reduce": (_I, [_P, _I]),
     "spc_agg_buffer": (_I, [_P, _I, ctypes.POINTER(_P), ctypes.POINTER(_I64), ctypes.POINTER(_P)]),
     "spc_finish_layer": (_I, [_P, _I]),
@@ -91,7 +95,11 @@ def lib() -> ctypes.CDLL:
             raise ImportError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
                               "(there is no CPU fallback for the SpeCache hot path)")
         handle = ctypes.CDLL(LIB_PATH)
+        # SPC_LIB_PATH points A/B tools at older builds, which may lack newer entries
+        lenient = "SPC_LIB_PATH" in os.environ
         for name, (res, args) in _SIGS.items():
+            if lenient and not hasattr(handle, name):
+                continue
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args

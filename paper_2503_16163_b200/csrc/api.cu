@@ -86,6 +86,7 @@ struct spc_cache {
     return sel_stream ? ((layer & 1) ? sel_stream2 : sel_stream) : cstream(layer);
   }
   float *part_o = nullptr, *part_ml = nullptr, *pin_ml = nullptr, *spill = nullptr, *mz = nullptr;
+  float* dbg_out = nullptr;  // spc_debug_output_f32: [layers][b][2][Hq][d] fp32 outputs
   int32_t* staging = nullptr;
   unsigned long long* pf_rows = nullptr;
   int context_length = 0;
@@ -94,6 +95,8 @@ struct spc_cache {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_attn, prof_sel, prof_wait, prof_pf;
+  cudaEvent_t prof_base = nullptr;  // recorded when profiling starts: common origin of the intervals
+  double last_pf_wall_ms = 0;
   int64_t launches = 0;
   double last_wait_ms = 0, last_pf_ms = 0;
   int64_t last_pf_rows = 0;
@@ -221,6 +224,7 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
   a.spill = c->spill + (size_t)layer * G.batch * G.Hq * (size_t)G.L;
   a.mz = c->mz + (size_t)layer * G.batch * G.Hq * 2;
   a.sm_scale_log2 = (float)(1.0 / std::sqrt((double)G.d) * 1.4426950408889634);
+  a.out_f32 = c->dbg_out ? c->dbg_out + (size_t)layer * G.batch * 2 * G.Hq * G.d : nullptr;
   bool fast = (c->impl != 1) && attend_fast_supported(G, rows);
   if (c->impl == 2 && !fast) return fail(SPC_EINVAL, "fast attention path not available for this geometry");
   cudaEvent_t p0 = nullptr, p1 = nullptr;
@@ -384,7 +388,7 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
     size_t off[16], tot = 0, sizes[16] = {codes, 0, kpar, vpar, ring, ring, pool, pool,
                                           b * U * G.k * 4, b * U * (G.L / 32) * 4, b * U * (size_t)G.L * 4,
                                           b * U * G.k * 4, b * U * 4, b * U * G.k * 4, b * U * G.k * 4,
-                                          b * H * 2 * 4};
+                                          b * H * 4 * 4};
     for (int i = 0; i < 16; ++i) {
       off[i] = tot;
       tot += align_up(std::max<size_t>(sizes[i], 16), 256);
@@ -493,9 +497,11 @@ int spc_cache_destroy(spc_cache* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (void* p : c->dev_allocs) cudaFree(p);
+  if (c->dbg_out) cudaFree(c->dbg_out);
   if (c->host_k) cudaFreeHost(c->host_k);
   if (c->host_v) cudaFreeHost(c->host_v);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->prof_base) cudaEventDestroy(c->prof_base);
   for (auto e : c->ev_agg) if (e) cudaEventDestroy(e);
   for (auto e : c->ev_sel) if (e) cudaEventDestroy(e);
   if (c->sel_stream) cudaStreamDestroy(c->sel_stream);
@@ -709,6 +715,31 @@ int spc_debug_agg(spc_cache* c, int layer, float* agg, void* stream) {
   return SPC_OK;
 }
 
+int spc_debug_output_f32(spc_cache* c, int enable) {
+  if (!c) return fail(SPC_EINVAL, "null cache");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (enable && !c->dbg_out) {
+    const size_t bytes = (size_t)c->G.layers * c->G.batch * 2 * c->G.Hq * c->G.d * sizeof(float);
+    CUDA_TRY(cudaMalloc((void**)&c->dbg_out, bytes));
+    CUDA_TRY(cudaMemset(c->dbg_out, 0, bytes));
+  } else if (!enable && c->dbg_out) {
+    CUDA_TRY(cudaFree(c->dbg_out));
+    c->dbg_out = nullptr;
+  }
+  return SPC_OK;
+}
+
+int spc_debug_out_f32(spc_cache* c, int layer, float* out, void* stream) {
+  if (int rc = check_layer(c, layer)) return rc;
+  if (!c->dbg_out) return fail(SPC_EINVAL, "spc_debug_out_f32 needs spc_debug_output_f32(cache, 1)");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t n = (size_t)c->G.batch * 2 * c->G.Hq * c->G.d;
+  CUDA_TRY(cudaMemcpyAsync(out, c->dbg_out + (size_t)layer * n, n * sizeof(float), cudaMemcpyDeviceToDevice,
+                           (cudaStream_t)stream));
+  return SPC_OK;
+}
+
 int spc_materialize(spc_cache* c, int layer, int seq, int head, float* keys, float* values, void* stream) {
   if (int rc = check_layer(c, layer)) return rc;
   if (seq < 0 || seq >= c->G.batch || head < 0 || head >= c->G.H) return fail(SPC_EINVAL, "seq/head out of range");
@@ -787,6 +818,29 @@ int spc_profile(spc_cache* c, int enable, double* attn_ms, int64_t* attn_launche
     pf += ms;
   }
   c->last_pf_ms = pf;
+  // wall time of the prefetch: union of the K5 intervals (two copy streams overlap)
+  c->last_pf_wall_ms = 0;
+  if (c->prof_base && !c->prof_pf.empty()) {
+    std::vector<std::pair<float, float>> iv;
+    for (auto& p : c->prof_pf) {
+      float s0 = 0, s1 = 0;
+      CUDA_TRY(cudaEventElapsedTime(&s0, c->prof_base, p.first));
+      CUDA_TRY(cudaEventElapsedTime(&s1, c->prof_base, p.second));
+      iv.push_back({s0, s1});
+    }
+    std::sort(iv.begin(), iv.end());
+    double tot = 0, a0 = iv[0].first, a1 = iv[0].second;
+    for (size_t i = 1; i < iv.size(); ++i) {
+      if (iv[i].first > a1) {
+        tot += a1 - a0;
+        a0 = iv[i].first;
+        a1 = iv[i].second;
+      } else {
+        a1 = std::max(a1, (double)iv[i].second);
+      }
+    }
+    c->last_pf_wall_ms = tot + (a1 - a0);
+  }
   unsigned long long rows = 0;
   CUDA_TRY(cudaMemcpy(&rows, c->pf_rows, sizeof(rows), cudaMemcpyDeviceToHost));
   CUDA_TRY(cudaMemset(c->pf_rows, 0, sizeof(rows)));
@@ -803,11 +857,57 @@ int spc_profile(spc_cache* c, int enable, double* attn_ms, int64_t* attn_launche
   c->ev_used = 0;
   c->launches = 0;
   c->prof = enable != 0;
+  if (c->prof) {
+    if (!c->prof_base) CUDA_TRY(cudaEventCreate(&c->prof_base));
+    CUDA_TRY(cudaEventRecord(c->prof_base, c->copy_stream));  // the device is idle (synchronized above)
+  }
   return SPC_OK;
 }
 
 double spc_profile_wait_ms(const spc_cache* c) { return c ? c->last_wait_ms : -1.0; }
 double spc_profile_prefetch_ms(const spc_cache* c) { return c ? c->last_pf_ms : -1.0; }
+double spc_profile_prefetch_wall_ms(const spc_cache* c) { return c ? c->last_pf_wall_ms : -1.0; }
+
+int spc_h2d_peak(int device, int64_t bytes, double* dma_gbs, double* zero_copy_gbs) {
+  if (bytes < (1 << 20) || bytes % 16) return fail(SPC_EINVAL, "spc_h2d_peak: bytes must be >= 1 MiB and a multiple of 16");
+  CUDA_TRY(cudaSetDevice(device));
+  void* h = nullptr;
+  void* dv = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int rc = SPC_OK;
+  auto best_of = [&](auto&& body) -> double {
+    double best = 0;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0, st);
+      body();
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms > 0) best = std::max(best, bytes / (ms * 1e-3) / 1e9);
+    }
+    return best;
+  };
+  if (cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaMalloc(&dv, bytes) != cudaSuccess || cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+    rc = fail(SPC_ENOMEM, "spc_h2d_peak: allocation failed");
+  } else {
+    std::memset(h, 1, bytes);
+    void* hd = nullptr;
+    cudaHostGetDevicePointer(&hd, h, 0);
+    if (dma_gbs) *dma_gbs = best_of([&] { cudaMemcpyAsync(dv, h, bytes, cudaMemcpyHostToDevice, st); });
+    if (zero_copy_gbs) *zero_copy_gbs = best_of([&] { launch_h2d_probe(hd, dv, (size_t)bytes, 2 * kNumSMs, st); });
+    if (cudaGetLastError() != cudaSuccess) rc = fail(SPC_ECUDA, "spc_h2d_peak: probe failed");
+  }
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  if (dv) cudaFree(dv);
+  if (h) cudaFreeHost(h);
+  return rc;
+}
 int64_t spc_profile_prefetch_bytes(const spc_cache* c) {
   // one new pin moves the K and V rows of the unit's heads (16-bit accounting, kvcache.py:148-150)
   return c ? c->last_pf_rows * (int64_t)2 * c->G.Hu * c->G.d * 2 : -1;

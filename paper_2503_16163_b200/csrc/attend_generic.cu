@@ -68,7 +68,9 @@ __global__ void k_combine(AttnArgs a) {
           o = fmaf(a.part_o[(base + (size_t)s * R + j) * G.d + c],
                    exp2f(a.part_ml[(base + (size_t)s * R + j) * 2] - M), o);
       }
-      a.out[(((size_t)b * a.rows + r) * G.Hq + hq) * G.d + c] = __float2bfloat16_rn(o * invL);
+      const size_t oi = (((size_t)b * a.rows + r) * G.Hq + hq) * G.d + c;
+      a.out[oi] = __float2bfloat16_rn(o * invL);
+      if (a.out_f32) a.out_f32[oi] = o * invL;
     }
     if (threadIdx.x == 0) {
       if (r == a.agg_row) {

@@ -88,6 +88,27 @@ constexpr float kSlack = (float)kSlackLog2;
 // and the scales by 2^aq, so both factors stay in the f16 normal range and
 // max |B| <= 2^14 as before.
 constexpr bool kHalfKeyB = SPC_K2_HKB != 0;
+#ifndef SPC_K2_VCOOP
+#define SPC_K2_VCOOP 1
+#endif
+// Cooperative value-parameter decode for the wide GQA rows (NR >= 4, SPC_K2_VCOOP):
+// once per block the 32 lanes decode the 128 (token, group) value params into
+// f16 hi + lo pairs of s' = s * 2^-(q+Ev) and z' = z * 2^-Ez in shared memory
+// (each lane one (group, k-step, tq): four tokens).  The value B fragment of
+// row j is then mul_hilo(P hi/lo, s' hi/lo) -- four f16x2 ops per token pair --
+// instead of decoding every (token, group) param in all eight row lanes, and
+// sum_t P * z runs on the tensor cores: one m16n8k16 with A rows 0-3 = z' hi of
+// the four groups, rows 4-7 = z' lo, and B = the P hi / lo fragments.
+constexpr bool kVCoop = SPC_K2_VCOOP != 0;
+#ifndef SPC_K2_CMMA
+#define SPC_K2_CMMA 1
+#endif
+// Zero-point constants on the tensor cores (NR >= 4 rows, SPC_K2_CMMA):
+// C_j = sum_c Q[j,c] z_c is one m16n8k16 per 16 channels with A = the CTA's
+// f16 hi + lo query table (rows 0-7 hi, 8-15 lo) and B = the block's key
+// zero-points z * 2^-Ezk as f16 hi + lo (columns 0, 1), instead of 32 FFMA and a
+// 9-shuffle reduce-scatter per lane and block.
+constexpr bool kCMma = SPC_K2_CMMA != 0;
 #ifndef SPC_K2_EXACT_ORDER
 #define SPC_K2_EXACT_ORDER 0
 #endif
@@ -124,13 +145,15 @@ __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__
 // (hi, lo) f16x2 of the product of two hi + lo f16x2 pairs (see kHalfKeyB)
 __device__ __forceinline__ void mul_hilo(uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl, uint32_t& hi,
                                          uint32_t& lo) {
-  const __half2 Ah = u2h(ah), Bh = u2h(bh);
-  const __half2 H = __hmul2_rn(Ah, Bh);
-  __half2 e = __hfma2(Ah, Bh, __hneg2(H));
-  e = __hfma2(Ah, u2h(bl), e);
-  e = __hfma2(u2h(al), Bh, e);
-  hi = h2u(H);
-  lo = h2u(e);
+  // hi = rn(ah*bh); lo = rn(al*bh + rn(ah*bl + (ah*bh - hi))) -- the first FMA is exact
+  asm("{\n\t.reg .b32 nh, e;\n\t"
+      "mul.rn.f16x2 %0, %2, %4;\n\t"
+      "neg.f16x2 nh, %0;\n\t"
+      "fma.rn.f16x2 e, %2, %4, nh;\n\t"
+      "fma.rn.f16x2 e, %2, %5, e;\n\t"
+      "fma.rn.f16x2 %1, %3, %4, e;\n\t}"
+      : "=r"(hi), "=r"(lo)
+      : "r"(ah), "r"(al), "r"(bh), "r"(bl));
 }
 
 __device__ __forceinline__ float fast_exp2(float x) {  // ex2.approx (|rel err| ~2^-22); -inf -> 0
@@ -255,6 +278,8 @@ struct MergeSmem {
   float o[kWarps][NR][128];
   float m[kWarps][NR];
   float l[kWarps][NR];
+  float f[kWarps][NR];  // exp2(m_w - M) per warp and row (0 for empty warps)
+  float M[NR], L[NR];
 };
 
 // exact segment scratch (split == nsplit CTAs): a chunk of CH full-precision
@@ -293,7 +318,7 @@ struct ExactRowsSmem {
 
 template <int BITS, int NR>
 constexpr size_t fast_smem_bytes() {
-  size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps + (NR > 2 ? NR * 32 * 16 * (kHalfKeyB ? 2 : 1) : 0), b = sizeof(MergeSmem<NR>),
+  size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps + (NR > 2 ? NR * 16 * (32 + (kHalfKeyB ? 36 : 0)) : 0), b = sizeof(MergeSmem<NR>),
          c = NR == 8 ? sizeof(ExactRowsSmem<NR>) : sizeof(ExactSmem<NR>);
   return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
@@ -835,7 +860,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   float Qr[QREG ? NR : 1][4];
   float4* Qs = reinterpret_cast<float4*>(smem_raw + kWarps * sizeof(WarpSmem<BITS, NR>));  // [NR][32]
   constexpr bool HKB = kHalfKeyB && !QREG;
-  uint4* Qh = reinterpret_cast<uint4*>(Qs + NR * 32);  // [NR][32] {Qhi b0, Qhi b1, Qlo b0, Qlo b1} (HKB)
+  // [NR][kQhS] {Qhi b0, Qhi b1, Qlo b0, Qlo b1} (HKB); row stride 36 keeps the C-MMA
+  // A-fragment loads (rows gq, gq + 1 in one 8-lane phase) conflict-free
+  constexpr int kQhS = 36;
+  uint4* Qh = reinterpret_cast<uint4*>(Qs + NR * 32);
   float qabs = 0.f;
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
@@ -870,12 +898,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
         split2(qq.x * sq, qq.z * sq, h.x, h.z);
         split2(qq.y * sq, qq.w * sq, h.y, h.w);
       }
-      Qh[j * 32 + lane] = h;
+      Qh[j * kQhS + lane] = h;
     }
   }
   if (!QREG) __syncthreads();
-  const float rk = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 2 + 0]) * cs;
-  const float rv = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 2 + 1]) * cs;
+  const float rk = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 4 + 0]) * cs;
+  const float rv = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 4 + 1]) * cs;
   const int Ek = (qabs * rk > 0.f) ? ceil_log2(qabs * rk) - 14 : 0;
   // lazy softmax rescale: P = exp2(s - m_run) may reach 2^kSlack, so the value
   // B exponent keeps kSlack bits of headroom (max|P*s'| <= 2^14 still)
@@ -884,11 +912,24 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   const float kscale = cs * pow2i(-sp - Ek + aq);         // (hi-lo) -> s * 2^(-sp-Ek) (* 2^aq: HKB)
   const float k_out = pow2i(24 + Ek);                     // D * k_out = sum_c code * Q * s
   const float v_out = pow2i(24 + Ev);
+  constexpr bool VCO = kVCoop && !PG;
+  // VCOOP: zero-points as f16 hi + lo of z * 2^-Ez, max |z * 2^-Ez| <= 2^14
+  const float rz = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 4 + 3]);
+  const int Ez = (VCO && rz > 0.f) ? ceil_log2(rz) - 14 : 0;
+  const float zsc = pow2i(-Ez), z_out = pow2i(Ez);
+  constexpr bool CMM = kCMma && HKB;
+  // C-MMA: key zero-points as f16 hi + lo of z * 2^-Ezk (max <= 2^14); D * 2^(Ezk + aq) = C_j
+  const float rzk = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 4 + 2]);
+  const int Ezk = (CMM && rzk > 0.f) ? ceil_log2(rzk) - 14 : 0;
+  const float zksc = pow2i(-Ezk), c_out = pow2i(Ezk + aq);
   float vscale[4];  // value K-index (token) scales, q = 2ks + khalf
 #pragma unroll
   for (int q = 0; q < 4; ++q) vscale[q] = cs * pow2i(-(BITS == 2 ? 2 * q : q) - Ev);
   // PG sz decode: this lane's ks = lane & 1 -> q = 2ks + khalf (kept in registers, no local array)
   const float vs_lane[2] = {(lane & 1) ? vscale[2] : vscale[0], (lane & 1) ? vscale[3] : vscale[1]};
+  // VCOOP decode role: lane = (group vg, k-step vks, tq); its tokens 16 vks + 2 tq + {0, 1, 8, 9}
+  const int vks = (lane >> 2) & 1;
+  const float vs_co[2] = {vks ? vscale[2] : vscale[0], vks ? vscale[3] : vscale[1]};
   // score rows of this lane and their spill rows (aggregate source)
   const int agg_j0 = a.agg_row * G.G;
   int jr[RPL];
@@ -973,9 +1014,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
       for (int j = 0; j < NR; ++j) {
         float q0, q1, q2, q3;
         if (HKB) {
-          const float4 qq = Qs[j * 32 + lane];
-          Cp[j] = fmaf(qq.x, z4[0], fmaf(qq.y, z4[1], fmaf(qq.z, z4[2], qq.w * z4[3])));
-          const uint4 qh = Qh[j * 32 + lane];
+          if (!CMM) {
+            const float4 qq = Qs[j * 32 + lane];
+            Cp[j] = fmaf(qq.x, z4[0], fmaf(qq.y, z4[1], fmaf(qq.z, z4[2], qq.w * z4[3])));
+          }
+          const uint4 qh = Qh[j * kQhS + lane];
           uint4 frag;
           mul_hilo(qh.x, qh.z, sh0, sl0, frag.x, frag.z);
           mul_hilo(qh.y, qh.w, sh1, sl1, frag.y, frag.w);
@@ -1006,26 +1049,43 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
         }
         ws.bk[kks][4 * j + (ktk ^ ((kks >> 1) & 3))] = frag;
       }
-      // reduce-scatter of the NR per-lane partials: after log2(NR) halving steps a
-      // lane holds one row, r = lane >> (5 - log2 NR); the remaining butterflies
-      // finish the sum (NR=8: 9 SHFL instead of 40)
-      constexpr int LG = NR == 1 ? 0 : NR == 2 ? 1 : NR == 4 ? 2 : 3;
-      float v[NR];
+      if constexpr (CMM) {
+        // this lane's key zero-points as f16 hi + lo pairs (same pairing as the Qh table)
+        // into the padding columns of bk: slot L = lane -> bk[L >> 2][4 NR + (L & 3)]
+        float zz[4];
 #pragma unroll
-      for (int j = 0; j < NR; ++j) v[j] = Cp[j];
-#pragma unroll
-      for (int st2 = 0; st2 < LG; ++st2) {
-        const int o = 16 >> st2, half = NR >> (st2 + 1);
-        const bool up = lane & o;
-#pragma unroll
-        for (int i2 = 0; i2 < half; ++i2) {
-          const float keep = up ? v[i2 + half] : v[i2], send = up ? v[i2] : v[i2 + half];
-          v[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        for (int m = 0; m < 4; ++m) zz[m] = z4[m] * zksc;
+        uint32_t zh0, zl0, zh1, zl1;
+        if (BITS == 2) {
+          split2(zz[0], zz[1], zh0, zl0);
+          split2(zz[2], zz[3], zh1, zl1);
+        } else {
+          split2(zz[0], zz[2], zh0, zl0);
+          split2(zz[1], zz[3], zh1, zl1);
         }
-      }
+        ws.bk[lane >> 2][4 * NR + (lane & 3)] = make_uint4(zh0, zh1, zl0, zl1);
+      } else {
+        // reduce-scatter of the NR per-lane partials: after log2(NR) halving steps a
+        // lane holds one row, r = lane >> (5 - log2 NR); the remaining butterflies
+        // finish the sum (NR=8: 9 SHFL instead of 40)
+        constexpr int LG = NR == 1 ? 0 : NR == 2 ? 1 : NR == 4 ? 2 : 3;
+        float v[NR];
 #pragma unroll
-      for (int o = 16 >> LG; o; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
-      Cp[0] = v[0];  // row (lane >> (5 - LG)) of this lane
+        for (int j = 0; j < NR; ++j) v[j] = Cp[j];
+#pragma unroll
+        for (int st2 = 0; st2 < LG; ++st2) {
+          const int o = 16 >> st2, half = NR >> (st2 + 1);
+          const bool up = lane & o;
+#pragma unroll
+          for (int i2 = 0; i2 < half; ++i2) {
+            const float keep = up ? v[i2 + half] : v[i2], send = up ? v[i2] : v[i2 + half];
+            v[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+#pragma unroll
+        for (int o = 16 >> LG; o; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+        Cp[0] = v[0];  // row (lane >> (5 - LG)) of this lane
+      }
     }
     // value params -> (s * 2^-(q+Ev), z) once per block: lane l decodes words 4l..4l+3
     // (group l>>3, tq (l>>1)&3, ks l&1, slots 0..3; slot>>1 = khalf -> q = 2ks + khalf)
@@ -1041,6 +1101,27 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
       }
       ws.sz[WarpSmem<BITS, NR>::szidx(2 * lane)] = make_float4(o[0], o[1], o[2], o[3]);
       ws.sz[WarpSmem<BITS, NR>::szidx(2 * lane + 1)] = make_float4(o[4], o[5], o[6], o[7]);
+    } else if constexpr (VCO) {
+      // lane = (vg = lane >> 3, vks, tq): words 32 vg + 8 tq + 4 vks + slot, slot = (t & 1) + 2 khalf
+      const uint4 vq = *reinterpret_cast<const uint4*>(S + SL::vp + 32 * (lane >> 3) + 8 * tq + 4 * vks);
+      const uint32_t w4[4] = {vq.x, vq.y, vq.z, vq.w};
+      float sv[4], zv[4];
+#pragma unroll
+      for (int slot = 0; slot < 4; ++slot) {
+        const float lo = __uint_as_float(w4[slot] << 16), hi = __uint_as_float(w4[slot] & 0xFFFF0000u);
+        sv[slot] = (hi - lo) * vs_co[slot >> 1];
+        zv[slot] = (BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo) * zsc;
+      }
+      uint4 sb, zh, zl;
+      split2(sv[0], sv[1], sb.x, sb.z);
+      split2(sv[2], sv[3], sb.y, sb.w);
+      split2(zv[0], zv[1], zh.x, zl.x);
+      split2(zv[2], zv[3], zh.y, zl.y);
+      uint4* vsb = reinterpret_cast<uint4*>(ws.sz);                // [vg][vks][tq] {sh01, sh89, sl01, sl89}
+      uint2* vza = reinterpret_cast<uint2*>(ws.sz + 32);           // [hl][vks][tq][vg] {z01, z89}
+      vsb[lane] = sb;
+      vza[(vks * 4 + tq) * 4 + (lane >> 3)] = make_uint2(zh.x, zh.y);
+      vza[32 + (vks * 4 + tq) * 4 + (lane >> 3)] = make_uint2(zl.x, zl.y);
     }
     // key codes of this lane's tokens T0 = 16mt + gq, T1 = T0 + 8
     uint32_t kw[2][2 * BITS];
@@ -1060,6 +1141,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
     }
     __syncwarp();
 
+    if constexpr (CMM) {  // C_j = sum_c Q[j,c] z_c: A = Qh rows (hi 0-7, lo 8-15), B = z (hi col 0, lo col 1)
+      float cacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) {
+        const uint4 qa = gq < NR ? Qh[gq * kQhS + 4 * kc + tq] : make_uint4(0u, 0u, 0u, 0u);
+        uint2 zb = make_uint2(0u, 0u);
+        if (gq < 2) zb = reinterpret_cast<const uint2*>(&ws.bk[kc][4 * NR + tq])[gq];
+        mma16816(cacc, qa.x, qa.z, qa.y, qa.w, zb.x, zb.y);
+      }
+      Cp[0] = ((cacc[0] + cacc[1]) + (cacc[2] + cacc[3])) * c_out;  // row gq (valid in lanes tq == 0)
+    }
     // ---- scores -------------------------------------------------------------------------
     float dk[2][4], dl[2][4];
 #pragma unroll
@@ -1119,7 +1211,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
       constexpr int LG = NR == 1 ? 0 : NR == 2 ? 1 : NR == 4 ? 2 : 3;
 #pragma unroll
       for (int e = 0; e < RPL; ++e)
-        cr[e] = __shfl_sync(0xffffffffu, Cp[0], (jr[e] & (NR - 1)) << (5 - LG));
+        cr[e] = __shfl_sync(0xffffffffu, Cp[0], CMM ? 4 * (jr[e] & (NR - 1)) : (jr[e] & (NR - 1)) << (5 - LG));
     }
     // sc[mt][hf][e]: token T = 16mt + gq + 8hf, row jr[e]
     float sc[2][2][RPL];
@@ -1194,8 +1286,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
         dv[mt][2] *= ac[0];
         dv[mt][3] *= ac[1];
       }
+      if (VCO) {  // z MMA accumulator: D columns = rows 2tq, 2tq+1 like dv
+        zacc[0] *= ac[0];
+        zacc[1] *= ac[1];
+        zacc[2 % (PG ? 1 : 4)] *= ac[0];
+        zacc[3 % (PG ? 1 : 4)] *= ac[1];
+      } else {
 #pragma unroll
-      for (int i = 0; i < (PG ? 1 : 4); ++i) zacc[i] *= az;
+        for (int i = 0; i < (PG ? 1 : 4); ++i) zacc[i] *= az;
+      }
     }
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
@@ -1309,6 +1408,38 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
     // shared by the four groups; per group and token only lo, hi, hi - lo and
     // two products remain.
     uint32_t vb[4][2][4];  // [grp][ks] {b0hi, b1hi, b0lo, b1lo}
+    if constexpr (VCO) {
+      // P pairs of this lane's row gq, tokens 16ks + 2tq + {0,1} (half 0) / {8,9} (half 1), f16 hi + lo
+      const bool live = gq < NR;
+      const int prow = live ? gq : 0;
+      uint32_t ph[2][2], pl[2][2];
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int hf2 = 0; hf2 < 2; ++hf2) {
+          const int t = 16 * ks + 2 * tq + 8 * hf2;
+          float p0 = ws.P[WarpSmem<BITS, NR>::pidx(prow, t)], p1 = ws.P[WarpSmem<BITS, NR>::pidx(prow, t + 1)];
+          if (!live) p0 = p1 = 0.f;
+          split2(p0, p1, ph[ks][hf2], pl[ks][hf2]);
+        }
+      // sum_t P z on the tensor cores (A rows 0-3 z' hi, 4-7 z' lo of the 4 groups, rows 8-15 zero)
+      const uint2* vza = reinterpret_cast<const uint2*>(ws.sz + 32);
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint2 za = vza[(gq >> 2) * 32 + (ks * 4 + tq) * 4 + (gq & 3)];
+        mma16816(zacc, za.x, 0u, za.y, 0u, ph[ks][0], ph[ks][1]);
+        mma16816(zacc, za.x, 0u, za.y, 0u, pl[ks][0], pl[ks][1]);
+      }
+      const uint4* vsb = reinterpret_cast<const uint4*>(ws.sz);
+#pragma unroll
+      for (int gi = 0; gi < 4; ++gi)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint4 sv = vsb[(gi * 2 + ks) * 4 + tq];
+          mul_hilo(ph[ks][0], pl[ks][0], sv.x, sv.z, vb[gi][ks][0], vb[gi][ks][2]);
+          mul_hilo(ph[ks][1], pl[ks][1], sv.y, sv.w, vb[gi][ks][1], vb[gi][ks][3]);
+        }
+    } else {
     {
       const int row = gq;
       const bool live = gq < NR;
@@ -1342,6 +1473,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
           split2(x[2], x[3], vb[gi][ks][1], vb[gi][ks][3]);
         }
       }
+    }
     }
     // value codes of this lane
     uint32_t vw[4 * BITS];
@@ -1413,10 +1545,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   }
 #pragma unroll
   for (int e = 0; e < RPL; ++e) l_run[e] = warp_sum_g(l_run[e]);
+  if (VCO) {  // z MMA: lanes gq (hi part) and gq + 4 (lo part) of group gq & 3
+    zacc[0] += __shfl_xor_sync(0xffffffffu, zacc[0], 16);
+    zacc[1] += __shfl_xor_sync(0xffffffffu, zacc[1], 16);
+  } else {
 #pragma unroll
-  for (int i = 0; i < (PG ? 1 : 4); ++i) {  // z sums over the 4 lanes of a row group
-    zacc[i] += __shfl_xor_sync(0xffffffffu, zacc[i], 1);
-    zacc[i] += __shfl_xor_sync(0xffffffffu, zacc[i], 2);
+    for (int i = 0; i < (PG ? 1 : 4); ++i) {  // z sums over the 4 lanes of a row group
+      zacc[i] += __shfl_xor_sync(0xffffffffu, zacc[i], 1);
+      zacc[i] += __shfl_xor_sync(0xffffffffu, zacc[i], 2);
+    }
   }
   __syncthreads();
   MergeSmem<NR>& ms = *reinterpret_cast<MergeSmem<NR>*>(smem_raw);
@@ -1451,8 +1588,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
     // columns = rows 2tq, 2tq+1; z sum of (grp, row j) lives in lanes gq == j
 #pragma unroll
     for (int gi = 0; gi < 4; ++gi) {
-      const float z0 = __shfl_sync(0xffffffffu, zacc[gi], 4 * (2 * tq));
-      const float z1 = __shfl_sync(0xffffffffu, zacc[gi], 4 * ((2 * tq + 1) & 7));
+      // VCO: lane (gq = gi, tq) holds group gi's z sums of rows 2tq, 2tq + 1 (scale 2^-Ez)
+      const float z0 = VCO ? __shfl_sync(0xffffffffu, zacc[0], 4 * gi + tq) * z_out
+                           : __shfl_sync(0xffffffffu, zacc[gi], 4 * (2 * tq));
+      const float z1 = VCO ? __shfl_sync(0xffffffffu, zacc[1], 4 * gi + tq) * z_out
+                           : __shfl_sync(0xffffffffu, zacc[gi], 4 * ((2 * tq + 1) & 7));
 #pragma unroll
       for (int mt = 2 * gi; mt < 2 * gi + 2; ++mt) {
 #pragma unroll
@@ -1468,26 +1608,34 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
     }
   }
   __syncthreads();
-  const size_t base = (((size_t)b * G.H + h) * (a.nsplit + 1) + split) * NR;
-  for (int i = threadIdx.x; i < NR * 128; i += kThreads) {
-    const int j = i >> 7, c = i & 127;
+  // merge factors once per (warp, row), then one FFMA per warp and element
+  if (threadIdx.x < NR) {
+    const int j = threadIdx.x;
     float M = -CUDART_INF_F;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w)
       if (ms.l[w][j] > 0.f) M = fmaxf(M, ms.m[w][j]);
-    float o = 0.f, L = 0.f;
+    float L = 0.f;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      if (ms.l[w][j] > 0.f) {
-        const float f = exp2f(ms.m[w][j] - M);
-        o = fmaf(ms.o[w][j][c], f, o);
-        L = fmaf(ms.l[w][j], f, L);
-      }
+      const float f = ms.l[w][j] > 0.f ? exp2f(ms.m[w][j] - M) : 0.f;
+      ms.f[w][j] = f;
+      L = fmaf(ms.l[w][j], f, L);
     }
+    ms.M[j] = M;
+    ms.L[j] = L;
+  }
+  __syncthreads();
+  const size_t base = (((size_t)b * G.H + h) * (a.nsplit + 1) + split) * NR;
+  for (int i = threadIdx.x; i < NR * 128; i += kThreads) {
+    const int j = i >> 7, c = i & 127;
+    float o = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) o = fmaf(ms.o[w][j][c], ms.f[w][j], o);
     a.part_o[(base + j) * 128 + c] = o;
     if (c == 0) {
-      a.part_ml[(base + j) * 2 + 0] = M;
-      a.part_ml[(base + j) * 2 + 1] = L;
+      a.part_ml[(base + j) * 2 + 0] = ms.M[j];
+      a.part_ml[(base + j) * 2 + 1] = ms.L[j];
     }
   }
 }

@@ -69,7 +69,7 @@ struct LayerBufs {
   int32_t* newcnt;     // [b][U]
   int32_t* fetch_slot; // [b][U][k]
   int32_t* fetch_pos;  // [b][U][k]
-  uint32_t* rmax;      // [b][H][2] max group range (hi-lo) of keys / values, fp32 bits
+  uint32_t* rmax;      // [b][H][4] fp32 bits: max group range (hi-lo) of keys, of values; max |key|; max |value|
   unsigned long long* pf_rows;  // cache-wide count of prefetched (new) pin rows (profiling)
 };
 

@@ -33,9 +33,11 @@ struct AttnArgs {
   float* spill;                // [b][Hq][L] agg-row logits, log2 domain
   float* mz;                   // [b][Hq][2] agg-row (max, sum), log2 domain
   float sm_scale_log2;         // d^-0.5 * log2(e)
+  float* out_f32;              // debug (spc_debug_output_f32): the combine's fp32 O before bf16 rounding
 };
 
 size_t quantize_smem_bytes(const Geo& G);
+void launch_h2d_probe(const void* src, void* dst, size_t bytes, int ctas, cudaStream_t st);
 void launch_quantize(const Geo& G, const LayerBufs& B, const QuantSrc& S, int blk0, int nblocks,
                      cudaStream_t st);
 void launch_export(const Geo& G, const LayerBufs& B, int seq, int nblocks, uint8_t* kc,

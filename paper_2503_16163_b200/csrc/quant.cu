@@ -53,10 +53,12 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
     return;
   }
 
-  __shared__ float s_rk, s_rv;
+  __shared__ float s_rk, s_rv, s_av, s_ak;
   if (tid == 0) {
     s_rk = 0.f;
     s_rv = 0.f;
+    s_av = 0.f;
+    s_ak = 0.f;
   }
   __syncthreads();
   // key groups: one per channel over the block's tokens (quant.py:163-169)
@@ -70,6 +72,7 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
     const uint32_t pw = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
     for (int r = 0; r < R; ++r) B.kparams[(bi + r) * G.rec + kpi(G, c)] = pw;  // every record of the group
     atomicMax(reinterpret_cast<unsigned*>(&s_rk), __float_as_uint(hi - lo));
+    atomicMax(reinterpret_cast<unsigned*>(&s_ak), __float_as_uint(fmaxf(fabsf(lo), fabsf(hi))));
     GroupParams p = params_from_minmax((double)lo, (double)hi, G.bits);
     kz[c] = p.zero;
     ks[c] = p.scale;
@@ -88,6 +91,7 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
     const int r = t / G.tb, tt = t - r * G.tb, s0 = vslot_of_group(G, j), s1 = vslot_of_group(G, j + 1);
     for (int sl = s0; sl < s1 && sl < G.vps; ++sl) B.vparams[(bi + r) * (size_t)G.rec + vpi(G, tt, sl)] = pw;
     atomicMax(reinterpret_cast<unsigned*>(&s_rv), __float_as_uint(hi - lo));
+    atomicMax(reinterpret_cast<unsigned*>(&s_av), __float_as_uint(fmaxf(fabsf(lo), fabsf(hi))));
     GroupParams p = params_from_minmax((double)lo, (double)hi, G.bits);
     vz[i] = p.zero;
     vs[i] = p.scale;
@@ -98,8 +102,10 @@ __global__ void __launch_bounds__(256) k_quantize(Geo G, LayerBufs B, QuantSrc S
   }
   __syncthreads();
   if (tid == 0) {  // per-(seq, head) range maxima: exponent choice of the MMA path
-    atomicMax(&B.rmax[((size_t)b * G.H + h) * 2 + 0], __float_as_uint(s_rk));
-    atomicMax(&B.rmax[((size_t)b * G.H + h) * 2 + 1], __float_as_uint(s_rv));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 0], __float_as_uint(s_rk));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 1], __float_as_uint(s_rv));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 3], __float_as_uint(s_av));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 2], __float_as_uint(s_ak));
   }
   for (int i = tid; i < g * d; i += nt) {
     int t = i / d, c = i - t * d, w, bit;
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
   __shared__ double kz64[d], ks64[d];
   __shared__ float vz[g * 4], vrs[g * 4], vthr[g * 4];
   __shared__ double vz64[g * 4], vs64[g * 4];
-  __shared__ float s_rk, s_rv;
+  __shared__ float s_rk, s_rv, s_av, s_ak;
   // ---- stage: 32 rows x 16 chunks of 16 bytes, for K and V
   for (int i = tid; i < g * 16; i += 256) {
     const int t = i >> 4, ch = i & 15;
@@ -177,6 +183,8 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
   if (tid == 0) {
     s_rk = 0.f;
     s_rv = 0.f;
+    s_av = 0.f;
+    s_ak = 0.f;
   }
   __syncthreads();
   const size_t bi = blk_index(G, b, h, blk);
@@ -195,6 +203,7 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
       }
       B.kparams[bi * G.rec + kpi(G, c)] = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
       atomicMax(reinterpret_cast<unsigned*>(&s_rk), __float_as_uint(hi - lo));
+      atomicMax(reinterpret_cast<unsigned*>(&s_ak), __float_as_uint(fmaxf(fabsf(lo), fabsf(hi))));
       gidx = c;
     } else {    // value group: 32 channels of token t (quant.py:177-186); rotated reads spread banks
       const int i = tid - 128, t = i >> 2, j = i & 3;
@@ -208,6 +217,7 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
       B.vparams[bi * (size_t)G.rec + vpi(G, t, j)] =
           float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
       atomicMax(reinterpret_cast<unsigned*>(&s_rv), __float_as_uint(hi - lo));
+      atomicMax(reinterpret_cast<unsigned*>(&s_av), __float_as_uint(fmaxf(fabsf(lo), fabsf(hi))));
       gidx = i;
     }
     const GroupParams p = params_from_minmax((double)lo, (double)hi, BITS);
@@ -228,8 +238,10 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
   }
   __syncthreads();
   if (tid == 0) {  // per-(seq, head) range maxima: exponent choice of the MMA path
-    atomicMax(&B.rmax[((size_t)b * G.H + h) * 2 + 0], __float_as_uint(s_rk));
-    atomicMax(&B.rmax[((size_t)b * G.H + h) * 2 + 1], __float_as_uint(s_rv));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 0], __float_as_uint(s_rk));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 1], __float_as_uint(s_rv));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 3], __float_as_uint(s_av));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 2], __float_as_uint(s_ak));
   }
   // Fast code of element x in its group: 1-bit x >= thr; 2-bit rint via the
   // 1.5*2^23 magic add (round-to-nearest-even, as rint) clipped to 3.  `near`

@@ -331,6 +331,25 @@ void launch_prefetch_one(const Geo& G, const LayerBufs& B, int seq, int unit,
   launch_pf(int64_t(256) << 10, 1, G, B, host_k, host_v, seq, unit, 1, st);
 }
 
+// Host-link peak probe (spc_h2d_peak): a zero-copy read of a contiguous pinned
+// buffer by `ctas` CTAs x 256 threads, 4 independent 16-byte loads per thread.
+__global__ void __launch_bounds__(256) k_h2d_probe(const uint4* __restrict__ src, uint4* __restrict__ dst, size_t n) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += 4 * stride) {
+    uint4 r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u * stride < n) r[u] = src[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u * stride < n) dst[i + u * stride] = r[u];
+  }
+}
+
+void launch_h2d_probe(const void* src, void* dst, size_t bytes, int ctas, cudaStream_t st) {
+  k_h2d_probe<<<ctas, 256, 0, st>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), bytes / 16);
+}
+
 // pin() with caller-supplied rows: device bf16 [npos][Hu][d] -> slots 0..npos-1
 __global__ void k_copy_pins(Geo G, LayerBufs B, int seq, int unit, const __nv_bfloat16* kr,
                             const __nv_bfloat16* vr) {

@@ -138,6 +138,18 @@ class SpeculativeLayerDecoder:
         _lib.check(_lib.lib().spc_debug_agg(c.handle, layer, agg.data_ptr(), current_stream(self._dev)))
         return agg
 
+    def debug_output_f32(self, enable: bool = True) -> None:
+        """Keep each layer's fp32 attention output (before the bf16 rounding) for parity tests."""
+        _lib.check(_lib.lib().spc_debug_output_f32(self.cache.handle, int(enable)))
+
+    def debug_out_f32(self, layer: int, rows: int):
+        """The last fp32 output of `layer`: [batch, rows, q_heads, head_dim]."""
+        import torch
+        c = self.cache
+        buf = torch.empty((c.batch, 2, c.q_heads, c.head_dim), dtype=torch.float32, device=self._dev)
+        _lib.check(_lib.lib().spc_debug_out_f32(c.handle, layer, buf.data_ptr(), current_stream(self._dev)))
+        return buf.view(-1)[:c.batch * rows * c.q_heads * c.head_dim].view(c.batch, rows, c.q_heads, c.head_dim)
+
 
 class _CudaArray:
     """__cuda_array_interface__ over library-owned device memory (zero copy)."""

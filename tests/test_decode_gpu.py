@@ -2,9 +2,13 @@
 reference itself (golden fixtures) and against the pinned oracle on seeded
 inputs (C1 geometry, GQA, per-kv-head scope).
 
-Tolerances (north star): outputs within 2e-3 relative -- the norm-relative
-error per (seq, row, q head) of the bf16 device output against the reference
-output rounded to bf16 (bf16 I/O), plus an elementwise bound of 4e-3 * max|O|;
+Tolerances (north star): outputs within 2e-3 relative (fp32 accumulate, bf16
+I/O).  Where the test reads the kernel's fp32 output before the bf16 rounding
+(spc_debug_out_f32) the bound is the norm-relative error per (seq, row, q head)
+of that fp32 output against the reference, and the bf16 output must be its
+round-to-nearest-even bit for bit; otherwise it is the per-head error of the
+bf16 output against the reference rounded to bf16.  Plus an elementwise bound
+of 4e-3 * max|O|;
 agg / pinned mass to 1e-4 relative (fp32 accumulation order); top-k sets
 identical except where the reference's own scores at the k / k+1 boundary
 are within 1e-4 relative (documented near-tie band)."""
@@ -26,32 +30,28 @@ def _dec(cache):
     return SpeculativeLayerDecoder(cache)
 
 
-def assert_out_close(got, exp):
-    """bf16 I/O: the device output is compared with the reference output
-    rounded to bf16 (the output rounding is part of the contract)."""
+def assert_out_close(got, exp, got32=None):
+    """bf16 I/O.  With got32 (the kernel's fp32 output before the bf16
+    rounding): per head ||got32 - exp|| / ||exp|| <= 2e-3 and got ==
+    bf16_rn(got32).  Without: the bf16 output against the reference rounded
+    to bf16 (the output rounding is part of the contract).  Returns the worst
+    per-head error."""
     got = np.asarray(got, np.float32).reshape(exp.shape[0], -1, exp.shape[-1])
     exp = exp.reshape(got.shape)
-    exp16 = R.bf16_round(exp)
+    if got32 is not None:
+        got32 = np.asarray(got32, np.float32).reshape(got.shape)
+        assert np.array_equal(got.view(np.uint32), R.bf16_round(got32).view(np.uint32)), "bf16 output != RN(fp32)"
+        cmp, ref = got32, exp
+    else:
+        cmp, ref = got, R.bf16_round(exp)
+    worst = 0.0
     for r in range(exp.shape[0]):
         for h in range(exp.shape[1]):
-            e = np.linalg.norm(got[r, h] - exp16[r, h]) / max(np.linalg.norm(exp[r, h]), 1e-30)
+            e = np.linalg.norm(cmp[r, h] - ref[r, h]) / max(np.linalg.norm(exp[r, h]), 1e-30)
+            worst = max(worst, e)
             assert e <= OUT_RTOL, f"row {r} head {h}: rel err {e:.2e}"
     assert np.abs(got - exp).max() <= 4e-3 * np.abs(exp).max()
-
-
-def assert_out_close_rows(got, exp):
-    """As assert_out_close, with the 2e-3 bound on each row's full attention
-    output (all heads) and 3e-3 per head (see test_long_run_ring_wrap_and_migrations)."""
-    got = np.asarray(got, np.float32).reshape(exp.shape[0], -1, exp.shape[-1])
-    exp = exp.reshape(got.shape)
-    exp16 = R.bf16_round(exp)
-    for r in range(exp.shape[0]):
-        e = np.linalg.norm(got[r] - exp16[r]) / max(np.linalg.norm(exp[r]), 1e-30)
-        assert e <= OUT_RTOL, f"row {r}: rel err {e:.2e}"
-        for h in range(exp.shape[1]):
-            e = np.linalg.norm(got[r, h] - exp16[r, h]) / max(np.linalg.norm(exp[r, h]), 1e-30)
-            assert e <= 1.5 * OUT_RTOL, f"row {r} head {h}: rel err {e:.2e}"
-    assert np.abs(got - exp).max() <= 4e-3 * np.abs(exp).max()
+    return worst
 
 
 def assert_topk_equivalent(got, exp, agg_ref, k):
@@ -78,8 +78,9 @@ def test_decode_layer_matches_reference_run(tag, impl):
     cache.set_attend_impl(impl)
     cache.prefill(0, K0[None], V0[None])
     dec = _dec(cache)
+    dec.debug_output_f32(True)
     out = dec.predecode_layer(0, z["pre_q"][None], z["pre_k"][None], z["pre_v"][None])
-    assert_out_close(out[0].float().cpu().numpy(), z["pre_out"])
+    assert_out_close(out[0].float().cpu().numpy(), z["pre_out"], dec.debug_out_f32(0, 1)[0].cpu().numpy())
     picked, newc = dec.ticket(0)
     f0 = R.frontier(n0, r, g)
     agg = dec.debug_agg(0)[0, 0, :f0].cpu().numpy()
@@ -90,7 +91,7 @@ def test_decode_layer_matches_reference_run(tag, impl):
     for i in range(steps):
         res = dec.decode_layer(0, i + 1, z["q"][i][None], z["k_new"][i][None], z["v_new"][i][None])
         torch.cuda.synchronize()
-        assert_out_close(res.out[0].float().cpu().numpy(), z["out"][i])
+        assert_out_close(res.out[0].float().cpu().numpy(), z["out"][i], dec.debug_out_f32(0, 2)[0].cpu().numpy())
         np.testing.assert_allclose(res.pinned_mass[0].cpu().numpy(), z["pinned_mass"][i],
                                    rtol=1e-4, atol=1e-6)
         n = n0 + i
@@ -108,7 +109,7 @@ def test_decode_layer_matches_reference_run(tag, impl):
     cache.close()
 
 
-def _oracle_run(cfg, seed, steps=3, impl="auto", per_row=False):
+def _oracle_run(cfg, seed, steps=3, impl="auto"):
     """Seeded C1-like run: device vs oracle for predecode + `steps` decode steps."""
     import torch
     from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
@@ -126,14 +127,16 @@ def _oracle_run(cfg, seed, steps=3, impl="auto", per_row=False):
     cache.set_attend_impl(impl)
     cache.prefill(0, np.stack([x[0] for x in KV]), np.stack([x[1] for x in KV]))
     dec = _dec(cache)
+    dec.debug_output_f32(True)
     q = np.stack([make_queries(rng, 1, Hq, d) for _ in range(b)])
     kn, vn = zip(*[make_step_kv(rng, 1, H, d) for _ in range(b)])
     kn, vn = np.stack(kn), np.stack(vn)
     out = dec.predecode_layer(0, q, kn, vn).float().cpu().numpy()
+    out32 = dec.debug_out_f32(0, 1).cpu().numpy()
     U = cache.units
     for s in range(b):
         o = R.predecode_layer(states[s], q[s], kn[s], vn[s])
-        assert_out_close(out[s], o["out"])
+        assert_out_close(out[s], o["out"], out32[s])
         picked, _ = dec.ticket(0)
         for u in range(U):
             got = [p for p in picked[s, u].tolist() if p >= 0]
@@ -146,14 +149,12 @@ def _oracle_run(cfg, seed, steps=3, impl="auto", per_row=False):
         res = dec.decode_layer(0, t, qcur, kn, vn)
         torch.cuda.synchronize()
         outs = res.out.float().cpu().numpy()
+        outs32 = dec.debug_out_f32(0, 2).cpu().numpy()
         pm = res.pinned_mass.cpu().numpy()
         picked, newc = dec.ticket(0)
         for s in range(b):
             o = R.decode_layer(states[s], qcur[s], kn[s], vn[s])
-            if per_row:
-                assert_out_close_rows(outs[s], o["out"])
-            else:
-                assert_out_close(outs[s], o["out"])
+            assert_out_close(outs[s], o["out"], outs32[s])
             np.testing.assert_allclose(pm[s], o["pinned_mass"], rtol=1e-4, atol=1e-6)
             for u in range(U):
                 got = [p for p in picked[s, u].tolist() if p >= 0]
@@ -344,15 +345,13 @@ def test_long_run_ring_wrap_and_migrations(H, Hq, bits):
     residual ring wraps and the frontier migrates twice mid-run.
 
     Every step must match the oracle: identical top-k sets (up to the near-tie
-    band), pinned mass, and outputs within 2e-3 of the bf16-rounded reference
-    for each row as a whole (all heads).  Per head the bound is 3e-3.  Over
-    70 x 16 x 2 head-rows, the per-head comparison of two bf16-rounded results
-    sees occasional 1-ulp flips.  The kernel's score arithmetic errs by about
-    1.5e-6 (the zero-point sum) plus 1e-6 (the hi/lo operand split).  The
-    reference's own fp32 scores err by 1.7e-6 against exact arithmetic
-    (tools/precision_probe.py), so these flips are rounding noise
-    on both sides, not a kernel error."""
-    _oracle_run((1, 700, H, Hq, 128, bits, 32, 32, 16, "layer"), seed=41 + bits, steps=70, per_row=True)
+    band), pinned mass, and per (row, head) outputs within 2e-3 -- measured on
+    the kernel's fp32 output (spc_debug_out_f32), whose bf16 rounding must equal
+    the bf16 output bit for bit.  (Round 1 compared the bf16 output with the
+    bf16-rounded reference and needed 3e-3 per head: over 70 x 16 x 2
+    head-rows a ~1e-6 score difference flips an occasional element to the
+    neighbouring bf16 value on one side only.)"""
+    _oracle_run((1, 700, H, Hq, 128, bits, 32, 32, 16, "layer"), seed=41 + bits, steps=70)
 
 
 @pytest.mark.parametrize("k,bits", [(50, 2), (1, 1)])
