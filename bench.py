@@ -442,6 +442,47 @@ def prefill_cache(cache, cfg, host_layers, s0, device, seed):
         torch.cuda.synchronize(device)
 
 
+TIE_BAND = 1e-4   # documented near-tie band of the top-k parity contract
+
+
+def topk_band_population(dec, layer: int, cfg: dict) -> dict:
+    """Live, after the timed region: for `layer`'s last ticket, the positions
+    outside the picked set whose aggregate lies within TIE_BAND of the k-th
+    picked value (the only places a top-k set may differ from the reference's),
+    summed over sequences and units."""
+    import torch
+    agg = dec.debug_agg(layer)
+    picked, _ = dec.ticket(layer)
+    f = dec.cache.quantized_frontier(layer)
+    agg = agg[..., :f]
+    sel = picked.long()
+    valid = sel >= 0
+    vals = torch.gather(agg, -1, sel.clamp(min=0))
+    kth = torch.where(valid, vals, torch.full_like(vals, float("inf"))).min(-1).values
+    # outside the picked set: invalid (-1) picks point at a padding column f
+    mask = torch.ones(agg.shape[:-1] + (f + 1,), dtype=torch.bool, device=agg.device)
+    mask.scatter_(-1, torch.where(valid, sel, torch.full_like(sel, f)), False)
+    near = ((agg >= kth[..., None] * (1 - TIE_BAND)) & mask[..., :f]).sum().item()
+    return {"band_positions_outside_set": int(near), "units": int(agg.shape[0] * agg.shape[1]),
+            "layer": layer}
+
+
+def parity_record(config: str) -> dict:
+    """The oracle parity run at this config's geometry (tests/test_bench_geometry_gpu.py),
+    as committed under profiles/: top-k band swaps and worst per-head error."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_parity_bench_geometry.json")) as fh:
+            d = json.load(fh)
+    except (OSError, ValueError):
+        return {}
+    rec = d.get({"c4": "c4_share8"}.get(config, config))
+    if not rec:
+        return {}
+    return {"oracle_check": "tests/test_bench_geometry_gpu.py (profiles/r2_parity_bench_geometry.json)",
+            "oracle_band_swaps": rec.get("topk_band_swaps"),
+            "oracle_worst_head_rel_err_fp32": rec.get("worst_head_rel_err_fp32")}
+
+
 def agg_reducer(cache, layers, device, group=None):
     """Per-layer cross-rank sum of the partial top-k aggregate for a KV-head
     sharded cache (shard.py): NCCL all-reduce on the layer's copy stream, then
@@ -563,6 +604,7 @@ def run_gpu_arm(args, cfg):
     pf_wall_ms = lib.spc_profile_prefetch_wall_ms(h)
     pf_bytes = int(lib.spc_profile_prefetch_bytes(h))
     _, newc = dec.ticket(L // 2)
+    band = topk_band_population(dec, 0, cfg)
     npin = int((picked0 >= 0).sum().item()) // max(1, cfg["batch"])
     new_frac = float(newc.float().mean().item()) / max(1, cfg["topk"])
     elapsed_ms = reduce_max(elapsed_ms, device)
@@ -688,6 +730,7 @@ def run_gpu_arm(args, cfg):
                        "other groups' decode; wall clock around synchronize, max over ranks"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
+        "topk_parity": {"band": TIE_BAND, **band, **parity_record(args.config)},
         "setup_s": setup_s,
         "cpu_baseline": cpu_base,
     }

@@ -101,13 +101,15 @@ constexpr bool kHalfKeyB = SPC_K2_HKB != 0;
 // the four groups, rows 4-7 = z' lo, and B = the P hi / lo fragments.
 constexpr bool kVCoop = SPC_K2_VCOOP != 0;
 #ifndef SPC_K2_CMMA
-#define SPC_K2_CMMA 1
+#define SPC_K2_CMMA 0
 #endif
 // Zero-point constants on the tensor cores (NR >= 4 rows, SPC_K2_CMMA):
 // C_j = sum_c Q[j,c] z_c is one m16n8k16 per 16 channels with A = the CTA's
 // f16 hi + lo query table (rows 0-7 hi, 8-15 lo) and B = the block's key
 // zero-points z * 2^-Ezk as f16 hi + lo (columns 0, 1), instead of 32 FFMA and a
-// 9-shuffle reduce-scatter per lane and block.
+// 9-shuffle reduce-scatter per lane and block.  Off by default: the A/B on one
+// box measured C3 K2 +1.7% against the FFMA form (the fragment loads and their
+// address arithmetic cost more issue slots than the FFMA chain they replace).
 constexpr bool kCMma = SPC_K2_CMMA != 0;
 #ifndef SPC_K2_EXACT_ORDER
 #define SPC_K2_EXACT_ORDER 0
@@ -259,10 +261,13 @@ struct __align__(16) WarpSmem {
   // in 132-float planes, conflict-free for both the score-side stores (t = c+gq,
   // row = 2tq+e) and the value-side loads (row = gq, t = c+2tq)
   // PG rows use stride 40 (even: token pairs load as float2; banks 8*row + t)
-  static constexpr int kPWords = NR * 4 <= 8 ? NR * 40 : 2 * 132;
+  // VCOOP rows (NR >= 4): [row][36]: score-side stores conflict-free (banks 8tq + 4e + gq + ...),
+  // value-side token pairs load as float2
+  static constexpr bool kPRow = kVCoop && NR * 4 > 8;
+  static constexpr int kPWords = NR * 4 <= 8 ? NR * 40 : kPRow ? NR * 36 : 2 * 132;
   float P[kPWords];
   __device__ static constexpr int pidx(int row, int t) {
-    return NR * 4 <= 8 ? row * 40 + t : (row & 1) * 132 + t * 4 + (row >> 1);
+    return NR * 4 <= 8 ? row * 40 + t : kPRow ? row * 36 + t : (row & 1) * 132 + t * 4 + (row >> 1);
   }
   float4 sz[64];                                          // value (s*2^-q, z) pairs, vparams order (szidx)
   uint64_t bar[kS];
@@ -1112,16 +1117,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
         sv[slot] = (hi - lo) * vs_co[slot >> 1];
         zv[slot] = (BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo) * zsc;
       }
-      uint4 sb, zh, zl;
+      uint4 sb, za;
       split2(sv[0], sv[1], sb.x, sb.z);
       split2(sv[2], sv[3], sb.y, sb.w);
-      split2(zv[0], zv[1], zh.x, zl.x);
-      split2(zv[2], zv[3], zh.y, zl.y);
-      uint4* vsb = reinterpret_cast<uint4*>(ws.sz);                // [vg][vks][tq] {sh01, sh89, sl01, sl89}
-      uint2* vza = reinterpret_cast<uint2*>(ws.sz + 32);           // [hl][vks][tq][vg] {z01, z89}
+      split2(zv[0], zv[1], za.x, za.y);
+      split2(zv[2], zv[3], za.z, za.w);
+      uint4* vsb = reinterpret_cast<uint4*>(ws.sz);       // [vg][vks][tq] {sh01, sh89, sl01, sl89}
+      // z A fragments [vks][tq][vg ^ swz(tq)] {zh01, zl01, zh89, zl89}: rows g (hi) and g + 8 (lo)
+      uint4* vza = reinterpret_cast<uint4*>(ws.sz + 32);
       vsb[lane] = sb;
-      vza[(vks * 4 + tq) * 4 + (lane >> 3)] = make_uint2(zh.x, zh.y);
-      vza[32 + (vks * 4 + tq) * 4 + (lane >> 3)] = make_uint2(zl.x, zl.y);
+      vza[vks * 16 + tq * 4 + ((lane >> 3) ^ ((tq >> 1) << 1))] = za;
     }
     // key codes of this lane's tokens T0 = 16mt + gq, T1 = T0 + 8
     uint32_t kw[2][2 * BITS];
@@ -1418,17 +1423,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
 #pragma unroll
         for (int hf2 = 0; hf2 < 2; ++hf2) {
           const int t = 16 * ks + 2 * tq + 8 * hf2;
-          float p0 = ws.P[WarpSmem<BITS, NR>::pidx(prow, t)], p1 = ws.P[WarpSmem<BITS, NR>::pidx(prow, t + 1)];
-          if (!live) p0 = p1 = 0.f;
-          split2(p0, p1, ph[ks][hf2], pl[ks][hf2]);
+          float2 pp = *reinterpret_cast<const float2*>(&ws.P[WarpSmem<BITS, NR>::pidx(prow, t)]);
+          if (!live) pp = make_float2(0.f, 0.f);
+          split2(pp.x, pp.y, ph[ks][hf2], pl[ks][hf2]);
         }
-      // sum_t P z on the tensor cores (A rows 0-3 z' hi, 4-7 z' lo of the 4 groups, rows 8-15 zero)
-      const uint2* vza = reinterpret_cast<const uint2*>(ws.sz + 32);
+      // sum_t P z on the tensor cores: A rows g = z' hi, g + 8 = z' lo of group g (lanes gq < 4;
+      // lanes gq >= 4 load group gq & 3 again and fill D rows 4-7 / 12-15, which are ignored)
+      const uint4* vza = reinterpret_cast<const uint4*>(ws.sz + 32);
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
-        const uint2 za = vza[(gq >> 2) * 32 + (ks * 4 + tq) * 4 + (gq & 3)];
-        mma16816(zacc, za.x, 0u, za.y, 0u, ph[ks][0], ph[ks][1]);
-        mma16816(zacc, za.x, 0u, za.y, 0u, pl[ks][0], pl[ks][1]);
+        const uint4 za = vza[ks * 16 + tq * 4 + ((gq & 3) ^ ((tq >> 1) << 1))];
+        mma16816(zacc, za.x, za.y, za.z, za.w, ph[ks][0], ph[ks][1]);
+        mma16816(zacc, za.x, za.y, za.z, za.w, pl[ks][0], pl[ks][1]);
       }
       const uint4* vsb = reinterpret_cast<const uint4*>(ws.sz);
 #pragma unroll
@@ -1545,9 +1551,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
   }
 #pragma unroll
   for (int e = 0; e < RPL; ++e) l_run[e] = warp_sum_g(l_run[e]);
-  if (VCO) {  // z MMA: lanes gq (hi part) and gq + 4 (lo part) of group gq & 3
-    zacc[0] += __shfl_xor_sync(0xffffffffu, zacc[0], 16);
-    zacc[1] += __shfl_xor_sync(0xffffffffu, zacc[1], 16);
+  if (VCO) {  // z MMA: D rows gq (z' hi) + gq + 8 (z' lo) of group gq, lanes gq < 4
+    zacc[0] += zacc[2 % (PG ? 1 : 4)];
+    zacc[1] += zacc[3 % (PG ? 1 : 4)];
   } else {
 #pragma unroll
     for (int i = 0; i < (PG ? 1 : 4); ++i) {  // z sums over the 4 lanes of a row group
