@@ -111,6 +111,12 @@ constexpr bool kVCoop = SPC_K2_VCOOP != 0;
 // box measured C3 K2 +1.7% against the FFMA form (the fragment loads and their
 // address arithmetic cost more issue slots than the FFMA chain they replace).
 constexpr bool kCMma = SPC_K2_CMMA != 0;
+#ifndef SPC_K2_NOSPILL
+#define SPC_K2_NOSPILL 0
+#endif
+// Measurement only (SPC_K2_NOSPILL=1 builds an A/B library whose aggregate is
+// invalid): K2 without the speculative-row logit spill, to price the spill.
+constexpr bool kNoSpill = SPC_K2_NOSPILL != 0;
 #ifndef SPC_K2_EXACT_ORDER
 #define SPC_K2_EXACT_ORDER 0
 #endif
@@ -1248,7 +1254,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a
     }
 #pragma unroll
     for (int e = 0; e < RPL; ++e) {
-      if (spr[e]) {  // aggregate-row logits (one writer per position: pinned ones by the exact segment)
+      if (!kNoSpill && spr[e]) {  // aggregate-row logits (one writer per position: pinned ones by the exact segment)
         float* sp = spr[e] + pos0 + gq;
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
