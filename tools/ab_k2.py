@@ -17,13 +17,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def child(config, steps):
+def child(config, steps, heads=0, batch=0):
     import torch
 
     import bench
     from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache, SpeculativeLayerDecoder
     cfg = dict(bench.CONFIGS[config])
     cfg["layers"] = 1
+    if heads:  # e.g. one rank's share of a head-sharded config: --heads 1 --batch 32 (C4 over 8)
+        g = cfg["q_heads"] // cfg["kv_heads"]
+        cfg["kv_heads"], cfg["q_heads"] = heads, heads * g
+    if batch:
+        cfg["batch"] = batch
     dev = "cuda:0"
     budget = CacheBudget(bits=cfg["bits"], group_size=cfg["group"], residual=cfg["residual"],
                          prefetch_k=cfg["topk"], context_length=cfg["ctx"] + steps + 80)
@@ -49,14 +54,16 @@ def main():
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--child", action="store_true")
+    ap.add_argument("--heads", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=0)
     a = ap.parse_args()
     if a.child:
-        return child(a.config, a.steps)
+        return child(a.config, a.steps, a.heads, a.batch)
     for r in range(a.rounds):
         for lib in a.libs:
             env = dict(os.environ, SPC_LIB_PATH=os.path.abspath(lib))
             out = subprocess.run([sys.executable, __file__, "--child", "--config", a.config, "--steps",
-                                  str(a.steps)], env=env, capture_output=True, text=True)
+                                  str(a.steps), "--heads", str(a.heads), "--batch", str(a.batch)], env=env, capture_output=True, text=True)
             line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-300:]
             print(f"round {r} {os.path.basename(lib)}: {line}", flush=True)
 
