@@ -93,11 +93,13 @@ void launch_combine(const AttnArgs& a, cudaStream_t st) {
 
 // K3b: agg[i] = sum over the unit's q heads of A_j[agg_row, i], i < f, in
 // ascending head order like np.sum(axis=0) (engine.py:317).
-__global__ void __launch_bounds__(256) k_agg(AttnArgs a) {
+__global__ void __launch_bounds__(kSideThreads, kSideMinBlocks) k_agg(AttnArgs a) {
   const Geo G = a.G;
   const int u = blockIdx.y, b = blockIdx.z;
   const int h0 = G.scope ? u * G.G : 0, h1 = G.scope ? (u + 1) * G.G : G.Hq;
-  __shared__ float sM[256], sI[256];
+  extern __shared__ float s_mi[];  // [heads] max, [heads] 1/sum
+  float* sM = s_mi;
+  float* sI = s_mi + (h1 - h0);
   for (int x = threadIdx.x; x < h1 - h0; x += blockDim.x) {
     sM[x] = a.mz[((size_t)b * G.Hq + h0 + x) * 2];
     sI[x] = 1.f / a.mz[((size_t)b * G.Hq + h0 + x) * 2 + 1];
@@ -124,7 +126,8 @@ void launch_agg(const AttnArgs& a, cudaStream_t st) {
     return e ? std::max(1, atoi(e)) : 2 * 148 * 4;
   }();
   const int blocks = std::min((a.f + 255) / 256, std::max(1, budget / (a.G.U * a.G.batch)));
-  k_agg<<<dim3(blocks, a.G.U, a.G.batch), 256, 0, st>>>(a);
+  const int heads = a.G.scope ? a.G.G : a.G.Hq;
+  k_agg<<<dim3(blocks, a.G.U, a.G.batch), kSideThreads, 2 * heads * sizeof(float), st>>>(a);
 }
 
 }  // namespace spc

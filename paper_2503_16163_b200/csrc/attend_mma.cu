@@ -790,8 +790,18 @@ __device__ void exact_segment_rows(const AttnArgs& a, const int split, const int
   }
 }
 
+#ifndef SPC_K2_GQA_MAXREG
+#define SPC_K2_GQA_MAXREG 0
+#endif
+// Register cap of the wide GQA instantiations (NR >= 4; 0 = the 2-CTA launch
+// bound's 128).  At <= 120 registers two resident K2 CTAs leave 4096 registers
+// of the SM free, so small side kernels can run beside them instead of waiting
+// for a K2 CTA to retire.
+template <int NR>
+constexpr int k2_maxreg() { return (SPC_K2_GQA_MAXREG > 0 && NR >= 4) ? SPC_K2_GQA_MAXREG : 128; }
+
 template <int BITS, int NR>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_attend_fast(AttnArgs a) {
+__global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   constexpr int kSt = stages_of<BITS, NR>();
   // PACK: score MMA columns n = 2*row + plane (hi/lo of each row side by side),
   //       one MMA per k-step and one score row per lane (row = lane & 3).

@@ -29,12 +29,22 @@
 // (quant.py:59-73) is reconstructed bit-exactly on device; the normative fp16
 // (zero, scale) is a direct float64->fp16 rounding of those (quant.py:150-160).
 #pragma once
+// Threads per CTA of the side kernels that run beside K2 on the copy and
+// selection streams (K3b aggregate, K5 PCIe gather).  128 with <= 32 registers
+// fits in the 4096 registers two 120-register K2 CTAs leave free on an SM
+// (SPC_K2_GQA_MAXREG=120), so they need not wait for a K2 CTA to retire.
+#ifndef SPC_SIDE_THREADS
+#define SPC_SIDE_THREADS 256
+#endif
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace spc {
+constexpr int kSideThreads = SPC_SIDE_THREADS;
+// launch-bound occupancy hint that caps the side kernels at 32 registers when narrow
+constexpr int kSideMinBlocks = kSideThreads <= 128 ? 16 : 1;
 
 struct Geo {
   int layers, batch, H, Hq, d, bits, g, r, k, L, scope, host_layers;

@@ -53,18 +53,46 @@ __device__ inline int block_exclusive_scan(int v, int* warp_sums, int* total) {
 // Radix select of the K largest of agg[0, f) (uint32 bit patterns of
 // non-negative fp32), ties to the lower position, written ascending to sel[].
 // Whole-CTA cooperative (kTopkThreads threads).
+//
+// Memory-level parallelism decides its speed (ncu, C4 rank share: 30% of the
+// stall samples were long-scoreboard and 29% LSU throttle): every pass reads
+// agg coalesced, 16 bytes per thread and four loads in flight, and the final
+// position-ordered selection runs per warp over contiguous 32-element steps
+// with ballots (round 1 gave each thread a private contiguous range: 32 cache
+// lines per warp load).
 __device__ void select_topk_cta(const uint32_t* __restrict__ agg, int f, int K, int* sel) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kW = kTopkThreads / 32;
   __shared__ int hist[256];
   __shared__ int warp_sums[32];
   __shared__ int s_total, s_digit, s_remaining;
+  __shared__ int w_gt[kW], w_eq[kW];
   uint32_t prefix = 0, pmask = 0;
   int remaining = K;
+  const bool vec = ((reinterpret_cast<uintptr_t>(agg) & 15) == 0);
+  const int f4 = vec ? (f >> 2) : 0;
+  const uint4* agg4 = reinterpret_cast<const uint4*>(agg);
   if (K > 0) {
     for (int shift = 24; shift >= 0; shift -= 8) {
       for (int i = tid; i < 256; i += kTopkThreads) hist[i] = 0;
       __syncthreads();
-      for (int i = tid; i < f; i += kTopkThreads) {
+      constexpr int U = 4;
+      for (int i0 = tid; i0 < f4; i0 += U * kTopkThreads) {
+        uint4 v4[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * kTopkThreads;
+          v4[u] = i < f4 ? agg4[i] : make_uint4(~0u, ~0u, ~0u, ~0u);  // ~0u: never matches a prefix of agg >= 0
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (i0 + u * kTopkThreads < f4 && (vv[e] & pmask) == prefix) atomicAdd(&hist[(vv[e] >> shift) & 255u], 1);
+        }
+      }
+      for (int i = 4 * f4 + tid; i < f; i += kTopkThreads) {
         uint32_t v = agg[i];
         if ((v & pmask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1);
       }
@@ -106,26 +134,39 @@ __device__ void select_topk_cta(const uint32_t* __restrict__ agg, int f, int K, 
   }
   const uint32_t T = prefix;
   const int need_eq = remaining;  // elements == T to take, lowest positions first
-  // selection in position order: thread owns a contiguous range
-  const int per = (f + kTopkThreads - 1) / kTopkThreads;
-  const int i0 = min(f, tid * per), i1 = min(f, i0 + per);
+  // selection in position order: warp w owns the contiguous range [w*per, (w+1)*per),
+  // walked in coalesced 32-element steps; ballots order the lanes within a step
+  const int per = ((f + kW - 1) / kW + 31) & ~31;
+  const int r0 = min(f, warp * per), r1 = min(f, r0 + per);
+  const unsigned lt = (1u << lane) - 1u;
   int n_gt = 0, n_eq = 0;
   if (K > 0)
-    for (int i = i0; i < i1; ++i) {
-      uint32_t v = agg[i];
-      n_gt += v > T;
-      n_eq += v == T;
+    for (int i = r0 + lane; i - lane < r1; i += 32) {
+      const uint32_t v = i < r1 ? agg[i] : 0u;
+      n_gt += __popc(__ballot_sync(0xffffffffu, i < r1 && v > T));
+      n_eq += __popc(__ballot_sync(0xffffffffu, i < r1 && v == T));
     }
-  int eq_before = block_exclusive_scan(n_eq, warp_sums, &s_total);
-  int take_eq = max(0, min(n_eq, need_eq - eq_before));
-  int my_sel = (K > 0) ? n_gt + take_eq : 0;
-  int out = block_exclusive_scan(my_sel, warp_sums, &s_total);
-  if (my_sel) {
-    int eq_seen = 0;
-    for (int i = i0; i < i1; ++i) {
-      uint32_t v = agg[i];
-      bool take = v > T || (v == T && eq_seen++ < take_eq);
-      if (take) sel[out++] = i;
+  if (lane == 0) {
+    w_gt[warp] = n_gt;
+    w_eq[warp] = n_eq;
+  }
+  __syncthreads();
+  if (K > 0) {
+    int eq_before = 0, out = 0;  // exclusive prefix over the warps before this one
+    for (int w = 0; w < warp; ++w) {
+      const int te = max(0, min(w_eq[w], need_eq - eq_before));
+      out += w_gt[w] + te;
+      eq_before += w_eq[w];
+    }
+    int eq_left = max(0, need_eq - eq_before);  // equal elements this warp may still take
+    for (int i = r0 + lane; i - lane < r1; i += 32) {
+      const uint32_t v = i < r1 ? agg[i] : 0u;
+      const unsigned beq = __ballot_sync(0xffffffffu, i < r1 && v == T);
+      const bool eq_take = ((beq >> lane) & 1u) && __popc(beq & lt) < eq_left;
+      const unsigned bt = __ballot_sync(0xffffffffu, (i < r1 && v > T) || eq_take);
+      if ((bt >> lane) & 1u) sel[out + __popc(bt & lt)] = i;
+      out += __popc(bt);
+      eq_left -= min(eq_left, __popc(beq));
     }
   }
   __syncthreads();
@@ -251,7 +292,7 @@ void launch_set_pins(const Geo& G, const LayerBufs& B, int seq, int unit, const 
 // tier ([pos][H][d]).
 
 template <int kPfUnroll>
-__global__ void __launch_bounds__(256) k_prefetch(Geo G, LayerBufs B, const uint4* host_k,
+__global__ void __launch_bounds__(kSideThreads, kSideMinBlocks) k_prefetch(Geo G, LayerBufs B, const uint4* host_k,
                                                   const uint4* host_v, int seq0, int unit0, int one) {
   const int bu_i = one ? 0 : blockIdx.y;
   const int u = one ? unit0 : bu_i % G.U, b = one ? seq0 : bu_i / G.U;
@@ -312,12 +353,12 @@ static void launch_pf(int64_t inflight, int units, const Geo& G, const LayerBufs
   const uint4* hk = reinterpret_cast<const uint4*>(host_k);
   const uint4* hv = reinterpret_cast<const uint4*>(host_v);
   const int64_t per = inflight / units;            // bytes per (seq, unit)
-  const int64_t cta2 = 256 * 32 * 2;               // one CTA at depth 2
+  const int64_t cta2 = kSideThreads * 32 * 2;      // one CTA at depth 2
   if (per >= cta2) {
     const int ctas = (int)(per / cta2 < 16 ? per / cta2 : 16);
-    k_prefetch<2><<<dim3(ctas, one ? 1 : units), 256, 0, st>>>(G, B, hk, hv, seq, unit, one);
+    k_prefetch<2><<<dim3(ctas, one ? 1 : units), kSideThreads, 0, st>>>(G, B, hk, hv, seq, unit, one);
   } else {
-    k_prefetch<1><<<dim3(1, one ? 1 : units), 256, 0, st>>>(G, B, hk, hv, seq, unit, one);
+    k_prefetch<1><<<dim3(1, one ? 1 : units), kSideThreads, 0, st>>>(G, B, hk, hv, seq, unit, one);
   }
 }
 
