@@ -526,6 +526,9 @@ def run_gpu_arm(args, cfg):
         threads = os.cpu_count() or 1
         cpu_base = cpu_reference_sample(cfg, threads, max(1, min(threads, 16)))
     gcfg, cfg = cfg, lcfg   # gcfg: the global workload; cfg: this rank's share
+    if args.compute_priority:
+        # the decode loop's stream above the library's selection streams (lowest priority)
+        torch.cuda.set_stream(torch.cuda.Stream(device, priority=args.compute_priority))
 
     W, K = args.warmup, args.steps
     total_steps = 2 * (W + K)  # device-timed pass + end-to-end pass
@@ -536,6 +539,8 @@ def run_gpu_arm(args, cfg):
     cache = DeviceTwoTierCache(cfg["layers"], cfg["kv_heads"], cfg["head_dim"], budget,
                                batch=cfg["batch"], q_heads=cfg["q_heads"], device=torch.device(device).index,
                                host_layers=host_layers)
+    if args.pf_inflight:
+        cache.set_prefetch_inflight(args.pf_inflight)
     reduce_layer = None
     if reduce_agg:
         from paper_2503_16163_b200.shard import allreduce_sum
@@ -704,6 +709,7 @@ def run_gpu_arm(args, cfg):
         "config": workload_config(gcfg, world, args, part),
         "rank_share": {"kv_heads": cfg["kv_heads"], "q_heads": cfg["q_heads"], "batch": cfg["batch"],
                        "host_layers": host_layers, "attention_impl": "fast" if cache.fast_path else "generic",
+                       "prefetch_inflight_bytes": args.pf_inflight or None,
                        "host_slabs_note": "layers l, l' with l = l' mod host_layers share one pinned slow-tier "
                                           "slab and are fed identical KV (host RAM); PCIe bytes unchanged"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -952,6 +958,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--host-layers", type=int, default=0)
+    ap.add_argument("--compute-priority", type=int, default=0,
+                    help="CUDA stream priority of the decode loop (negative = higher; 0 = default stream priority)")
+    ap.add_argument("--pf-inflight", type=int, default=0,
+                    help="PCIe gather bytes in flight (spc_set_prefetch_inflight; 0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", default="auto", choices=["auto", "heads", "seq", "replicas"],
                     help="multi-GPU partition of the global batch: auto = by KV head, then by sequence "

@@ -59,6 +59,16 @@ namespace {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 int64_t frontier_of(int64_t n, int r, int g) { return n < r ? 0 : (int64_t)g * ((n - r) / g); }
 constexpr int kSplitCap = 128;
+// Measurement only: SPC_DEBUG_SKIP bitmask skips side kernels of the decode
+// layer (1 = K3b aggregate, 2 = K4 top-k, 4 = K5 PCIe gather) to price their
+// interference with K2 in the layer loop.  Results are invalid when set.
+int debug_skip() {
+  static const int v = [] {
+    const char* e = getenv("SPC_DEBUG_SKIP");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
 constexpr int kNumSMs = 148;
 }  // namespace
 
@@ -262,7 +272,7 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
     p0 = prof_event(c);
     CUDA_TRY(cudaEventRecord(p0, cs));
   }
-  launch_agg(a, cs);
+  if (!(debug_skip() & 1)) launch_agg(a, cs);
   c->launches += a.f > 0;
   CUDA_TRY(cudaGetLastError());
   if (c->agg_ext) {  // the caller reduces agg across ranks on cs, then spc_finish_layer
@@ -280,7 +290,7 @@ int ticket_tail(spc_cache* c, int layer, int f, int n_before, bool append_row0, 
   cudaEvent_t p1 = nullptr;
   if (c->prof) p1 = prof_event(c);
   cudaStream_t ss = c->sstream(layer);
-  launch_topk(G, c->L[layer], f, ss);
+  if (!(debug_skip() & 2)) launch_topk(G, c->L[layer], f, ss);
   if (ss != cs) {
     CUDA_TRY(cudaEventRecord(c->ev_sel[layer], ss));
     CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_sel[layer], 0));
@@ -291,8 +301,9 @@ int ticket_tail(spc_cache* c, int layer, int f, int n_before, bool append_row0, 
     q1 = prof_event(c);
     CUDA_TRY(cudaEventRecord(q0, cs));
   }
-  launch_prefetch(G, c->L[layer], host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer), c->pf_inflight,
-                  cs);
+  if (!(debug_skip() & 4))
+    launch_prefetch(G, c->L[layer], host_slab(c, c->host_k, layer), host_slab(c, c->host_v, layer), c->pf_inflight,
+                    cs);
   if (c->prof) {
     CUDA_TRY(cudaEventRecord(q1, cs));
     c->prof_pf.push_back({q0, q1});

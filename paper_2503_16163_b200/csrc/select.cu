@@ -313,6 +313,13 @@ __global__ void __launch_bounds__(kSideThreads, kSideMinBlocks) k_prefetch(Geo G
     }
     return;
   }
+  // the unit's (slot, position) list into shared memory first: the gather loop's
+  // host loads then depend on a shared-memory read, not on an HBM round trip
+  // each (k <= 1024 new pins: 8 KB)
+  __shared__ int2 s_sp[1024];
+  for (int i = threadIdx.x; i < nnew; i += blockDim.x)
+    s_sp[i] = make_int2(B.fetch_slot[bu * G.k + i], B.fetch_pos[bu * G.k + i]);
+  __syncthreads();
   const int vec = G.Hu * G.d / 8;  // uint4 per row
   const int total = nnew * vec;
   uint4* pk = reinterpret_cast<uint4*>(B.pool_k);
@@ -326,9 +333,9 @@ __global__ void __launch_bounds__(kSideThreads, kSideMinBlocks) k_prefetch(Geo G
       const int x = x0 + u2 * stride;
       if (x < total) {
         const int i = x / vec, e = x - i * vec;
-        const int slot = B.fetch_slot[bu * G.k + i], pos = B.fetch_pos[bu * G.k + i];
-        const size_t src = (((size_t)b * G.L + pos) * G.H + h0) * G.d / 8 + e;
-        dst[u2] = ((bu * G.k + slot) * G.Hu) * G.d / 8 + e;
+        const int2 sp = s_sp[i];
+        const size_t src = (((size_t)b * G.L + sp.y) * G.H + h0) * G.d / 8 + e;
+        dst[u2] = ((bu * G.k + sp.x) * G.Hu) * G.d / 8 + e;
         rk[u2] = host_k[src];
         rv[u2] = host_v[src];
       }
@@ -358,7 +365,7 @@ static void launch_pf(int64_t inflight, int units, const Geo& G, const LayerBufs
     const int ctas = (int)(per / cta2 < 16 ? per / cta2 : 16);
     k_prefetch<2><<<dim3(ctas, one ? 1 : units), kSideThreads, 0, st>>>(G, B, hk, hv, seq, unit, one);
   } else {
-    k_prefetch<1><<<dim3(1, one ? 1 : units), kSideThreads, 0, st>>>(G, B, hk, hv, seq, unit, one);
+    k_prefetch<4><<<dim3(1, one ? 1 : units), kSideThreads, 0, st>>>(G, B, hk, hv, seq, unit, one);
   }
 }
 
