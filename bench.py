@@ -621,44 +621,58 @@ def run_gpu_arm(args, cfg):
     # region copies them H2D, runs the step, and reads the results back
     e2e_in = [(q[i].cpu().pin_memory(), k_new[i].cpu().pin_memory(), v_new[i].cpu().pin_memory())
               for i in range(t, t + W + K)]
-    o_h = torch.empty_like(out, device="cpu").pin_memory()
-    pm_h = torch.empty_like(pm, device="cpu").pin_memory()
-    q_d, k_d, v_d = torch.empty_like(q[0]), torch.empty_like(k_new[0]), torch.empty_like(v_new[0])
+    # two buffer sets: step i+1's inputs copy in while step i decodes, and step
+    # i's results copy out while step i+1 decodes (each set is reused two steps later)
+    o_h = [torch.empty_like(out, device="cpu").pin_memory() for _ in range(2)]
+    pm_h = [torch.empty_like(pm, device="cpu").pin_memory() for _ in range(2)]
+    q_d = [torch.empty_like(q[0]) for _ in range(2)]
+    k_d = [torch.empty_like(k_new[0]) for _ in range(2)]
+    v_d = [torch.empty_like(v_new[0]) for _ in range(2)]
+    o_d = [out, torch.empty_like(out)]
+    pm_d = [pm, torch.empty_like(pm)]
 
-    # layer-pipelined: layer l+1's inputs copy H2D on one copy stream while layer
-    # l decodes, and layer l's outputs copy D2H on another; the step ends when
-    # its last results are on the host (the compute stream waits for them)
+    # layer-pipelined: layer group g+1's inputs copy H2D on one copy stream while
+    # group g decodes, and group g's outputs copy D2H on another
     comp = torch.cuda.current_stream(device)
     cs_in, cs_out = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    done_in = [None, None]   # compute finished reading input set s (event)
+    done_out = [None, None]  # output set s copied to the host (event)
 
     GRP = 8  # layers per copy group: one H2D and one D2H per group keeps the host-side cost low
 
     def step_e2e(i, tt):
+        sb = i & 1
         qh, kh, vh = e2e_in[i]
         groups = [(g0, min(L, g0 + GRP)) for g0 in range(0, L, GRP)]
         ev_in = [torch.cuda.Event() for _ in groups]
-        cs_in.wait_stream(comp)  # the previous step is done with q_d / k_d / v_d
+        if done_in[sb] is not None:
+            cs_in.wait_event(done_in[sb])  # step i-2 is done with this input set
         with torch.cuda.stream(cs_in):
             for gi, (g0, g1) in enumerate(groups):
-                q_d[g0:g1].copy_(qh[g0:g1], non_blocking=True)
-                k_d[g0:g1].copy_(kh[g0:g1], non_blocking=True)
-                v_d[g0:g1].copy_(vh[g0:g1], non_blocking=True)
+                q_d[sb][g0:g1].copy_(qh[g0:g1], non_blocking=True)
+                k_d[sb][g0:g1].copy_(kh[g0:g1], non_blocking=True)
+                v_d[sb][g0:g1].copy_(vh[g0:g1], non_blocking=True)
                 ev_in[gi].record(cs_in)
+        if done_out[sb] is not None:
+            comp.wait_event(done_out[sb])  # step i-2's results are on the host
         for gi, (g0, g1) in enumerate(groups):
             comp.wait_event(ev_in[gi])
             for layer in range(g0, g1):
-                _lib.check(lib.spc_decode_layer(h, layer, tt, q_d[layer].data_ptr(), k_d[layer].data_ptr(),
-                                                v_d[layer].data_ptr(), out[layer].data_ptr(),
-                                                pm[layer].data_ptr(), stream))
+                _lib.check(lib.spc_decode_layer(h, layer, tt, q_d[sb][layer].data_ptr(), k_d[sb][layer].data_ptr(),
+                                                v_d[sb][layer].data_ptr(), o_d[sb][layer].data_ptr(),
+                                                pm_d[sb][layer].data_ptr(), stream))
                 if reduce_layer:
                     reduce_layer(layer)
             ev = torch.cuda.Event()
             ev.record(comp)
             cs_out.wait_event(ev)
             with torch.cuda.stream(cs_out):
-                o_h[g0:g1].copy_(out[g0:g1], non_blocking=True)
-                pm_h[g0:g1].copy_(pm[g0:g1], non_blocking=True)
-        comp.wait_stream(cs_out)
+                o_h[sb][g0:g1].copy_(o_d[sb][g0:g1], non_blocking=True)
+                pm_h[sb][g0:g1].copy_(pm_d[sb][g0:g1], non_blocking=True)
+        done_in[sb] = torch.cuda.Event()
+        done_in[sb].record(comp)
+        done_out[sb] = torch.cuda.Event()
+        done_out[sb].record(cs_out)
 
     for i in range(W):
         step_e2e(i, t)
@@ -673,8 +687,8 @@ def run_gpu_arm(args, cfg):
     torch.cuda.synchronize(device)
     e2e_s = time.perf_counter() - w0
     e2e_s = reduce_max(e2e_s, device)
-    h2d = (q_d.numel() + k_d.numel() + v_d.numel()) * 2
-    d2h = o_h.numel() * 2 + pm_h.numel() * 4
+    h2d = (q_d[0].numel() + k_d[0].numel() + v_d[0].numel()) * 2
+    d2h = o_h[0].numel() * 2 + pm_h[0].numel() * 4
 
     ms_per_step = elapsed_ms / K
     # strong partition: the ranks together decode the global batch per step;
@@ -733,7 +747,8 @@ def run_gpu_arm(args, cfg):
                 "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "how": "through spc_decode_layer (C ABI) with pinned host inputs/outputs; per group of 8 "
                        "layers, H2D of its q/k/v and D2H of its outputs on two copy streams overlapping the "
-                       "other groups' decode; wall clock around synchronize, max over ranks"},
+                       "other groups' decode, two buffer sets so consecutive steps' copies overlap too; "
+                       "wall clock around synchronize, max over ranks"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "topk_parity": {"band": TIE_BAND, **band, **parity_record(args.config)},

@@ -6,6 +6,8 @@
 // kvcache.py:222-243 (materialize), kvcache.py:270-281 (snapshot).
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -325,6 +327,212 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
   }
 }
 
+// K1 v2 (round 2): the same bit-exact codes and layout as k_quantize_fast with
+// about half the instructions (ncu r1: 8.9k warp-instructions per block, 76%
+// issue-active; three shared-memory loads and the inverted (t, c) index math
+// per element were the bulk, the 4-way bank conflicts of the fp32 staging a
+// symptom).
+//  * rows are staged as raw bf16 with 16-byte stores (272-byte rows:
+//    conflict-free), not converted to fp32;
+//  * group (min, max) and the float64 parameters as before;
+//  * codes elementwise: thread (c = tid & 127) keeps its key channel's
+//    parameters in registers and walks 16 tokens; value parameters are
+//    warp-uniform broadcasts; one byte per code into shared memory (key codes
+//    [t][c], value codes [c][t] with 36-byte rows, both conflict-free);
+//  * words from bytes: a key word is one 16-byte (2-bit) / 2 x 16-byte (1-bit)
+//    load and a shift/mask gather; a value word reads its 8 / 16 (token pair)
+//    16-bit code pairs of the MMA-fragment layout (vloc).
+template <int BITS>
+__global__ void __launch_bounds__(256) k_quantize_fast2(Geo G, LayerBufs B, QuantSrc S, int blk0) {
+  constexpr int g = 32, d = 128, LD = 136;  // bf16 tile rows: 272 B = 68 words
+  const int blk = blk0 + blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
+  __shared__ __align__(16) uint16_t tk[g * LD];
+  __shared__ __align__(16) uint16_t tv[g * LD];
+  __shared__ __align__(16) uint8_t ck[g * d];   // key codes [t][c]
+  __shared__ __align__(16) uint8_t cv[d * 34];  // value codes [c][t], 34-byte rows (17 words: odd)
+  __shared__ float kz[d], krs[d], kthr[d];
+  __shared__ double kz64[d], ks64[d];
+  __shared__ float vz[g * 4], vrs[g * 4], vthr[g * 4];
+  __shared__ double vz64[g * 4], vs64[g * 4];
+  __shared__ float s_rk, s_rv, s_av, s_ak;
+  auto bf = [](uint16_t u) { return __uint_as_float((uint32_t)u << 16); };
+  // ---- stage: 32 rows x 16 chunks of 16 bytes, for K and V (raw bf16)
+  for (int i = tid; i < g * 16; i += 256) {
+    const int t = i >> 4, ch = i & 15;
+    const long long pos = (long long)blk * g + t;
+    const long long row = S.ring ? pos % S.ring : pos;
+    const long long off = b * S.seq_stride + row * S.tok_stride + (long long)h * S.head_stride + ch * 8;
+    *reinterpret_cast<uint4*>(tk + t * LD + ch * 8) = *reinterpret_cast<const uint4*>(S.k + off);
+    *reinterpret_cast<uint4*>(tv + t * LD + ch * 8) = *reinterpret_cast<const uint4*>(S.v + off);
+  }
+  if (tid == 0) {
+    s_rk = 0.f;
+    s_rv = 0.f;
+    s_av = 0.f;
+    s_ak = 0.f;
+  }
+  __syncthreads();
+  const size_t bi = blk_index(G, b, h, blk);
+  // ---- group parameters (quant.py:59-73 via :163-186): threads 0-127 a key
+  // group (channel c over the 32 tokens), threads 128-255 a value group
+  {
+    float lo, hi;
+    int gidx;
+    const bool key = tid < 128;
+    if (key) {
+      const int c = tid;
+      lo = hi = bf(tk[c]);
+#pragma unroll 8
+      for (int t = 1; t < g; ++t) {
+        const float x = bf(tk[t * LD + c]);
+        lo = fminf(lo, x);
+        hi = fmaxf(hi, x);
+      }
+      B.kparams[bi * G.rec + kpi(G, c)] = float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+      atomicMax(reinterpret_cast<unsigned*>(&s_rk), __float_as_uint(hi - lo));
+      atomicMax(reinterpret_cast<unsigned*>(&s_ak), __float_as_uint(fmaxf(fabsf(lo), fabsf(hi))));
+      gidx = c;
+    } else {  // 32 channels of token t, rotated start
+      const int i = tid - 128, t = i >> 2, j = i & 3;
+      const uint16_t* r = tv + t * LD + 32 * j;
+      lo = hi = bf(r[j]);
+#pragma unroll 8
+      for (int k = 1; k < 32; ++k) {
+        const float x = bf(r[(k + j) & 31]);
+        lo = fminf(lo, x);
+        hi = fmaxf(hi, x);
+      }
+      B.vparams[bi * (size_t)G.rec + vpi(G, t, j)] =
+          float_to_bf16_bits_exact(lo) | (float_to_bf16_bits_exact(hi) << 16);
+      atomicMax(reinterpret_cast<unsigned*>(&s_rv), __float_as_uint(hi - lo));
+      atomicMax(reinterpret_cast<unsigned*>(&s_av), __float_as_uint(fmaxf(fabsf(lo), fabsf(hi))));
+      gidx = i;
+    }
+    const GroupParams p = params_from_minmax((double)lo, (double)hi, BITS);
+    float thr = CUDART_INF_F, rs = 0.f, zf = 0.f;
+    if (p.scale != 0.0) {
+      if (BITS == 1) {
+        thr = __double2float_ru(__dadd_rn(p.zero, __ddiv_rn(p.scale, 2.0)));
+      } else {
+        zf = (float)p.zero;  // = lo, exact
+        rs = (float)(1.0 / p.scale);
+      }
+    }
+    if (key) {
+      kz[gidx] = zf; krs[gidx] = rs; kthr[gidx] = thr; kz64[gidx] = p.zero; ks64[gidx] = p.scale;
+    } else {
+      vz[gidx] = zf; vrs[gidx] = rs; vthr[gidx] = thr; vz64[gidx] = p.zero; vs64[gidx] = p.scale;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {  // per-(seq, head) range maxima: exponent choice of the MMA path
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 0], __float_as_uint(s_rk));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 1], __float_as_uint(s_rv));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 3], __float_as_uint(s_av));
+    atomicMax(&B.rmax[((size_t)b * G.H + h) * 4 + 2], __float_as_uint(s_ak));
+  }
+  // fast code: see k_quantize_fast (1-bit: x >= thr exact; 2-bit: fp32 rint with a
+  // float64 redo within 1e-5 of a rounding boundary)
+  // In-group values give q = (x - z) / s in [0, 3], so "within 1e-5 of a .5
+  // boundary" is |q - rint(q)| > 0.5 - 1e-5; written as !(<=) so that a NaN or
+  // infinite q (1/s overflowing fp32 for subnormal-range scales) also takes the
+  // float64 path.
+  auto fast_code = [&](float x, float z, float rs, float thr, bool& near) -> uint32_t {
+    if (BITS == 1) return x >= thr ? 1u : 0u;
+    const float dq = (x - z) * rs;
+    const float y = dq + 12582912.0f;
+    near = !(fabsf(dq - (y - 12582912.0f)) <= 0.49999f);
+    return min(__float_as_uint(y) & 0x3FFFFFu, 3u);
+  };
+  // ---- codes, one byte each, channel pairs (32-bit loads); the rare float64
+  // redo is taken once per warp
+  {
+    const int c = 2 * (tid & 63), t0 = tid >> 6, j = c >> 5;
+    const float z0 = kz[c], rs0 = krs[c], thr0 = kthr[c], z1 = kz[c + 1], rs1 = krs[c + 1], thr1 = kthr[c + 1];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = t0 + 4 * k;
+      const int gi = t * 4 + j;
+      const uint32_t uk = *reinterpret_cast<const uint32_t*>(tk + t * LD + c);
+      const uint32_t uv = *reinterpret_cast<const uint32_t*>(tv + t * LD + c);
+      const float xk0 = __uint_as_float(uk << 16), xk1 = __uint_as_float(uk & 0xFFFF0000u);
+      const float xv0 = __uint_as_float(uv << 16), xv1 = __uint_as_float(uv & 0xFFFF0000u);
+      const float vzz = vz[gi], vrr = vrs[gi], vth = vthr[gi];
+      bool n0 = false, n1 = false, n2 = false, n3 = false;
+      uint32_t k0 = fast_code(xk0, z0, rs0, thr0, n0), k1 = fast_code(xk1, z1, rs1, thr1, n1);
+      uint32_t v0 = fast_code(xv0, vzz, vrr, vth, n2), v1 = fast_code(xv1, vzz, vrr, vth, n3);
+      if (BITS == 2 && __any_sync(0xffffffffu, n0 || n1 || n2 || n3)) {
+        if (n0) k0 = quantize_code(xk0, GroupParams{kz64[c], ks64[c]}, 2);
+        if (n1) k1 = quantize_code(xk1, GroupParams{kz64[c + 1], ks64[c + 1]}, 2);
+        if (n2) v0 = quantize_code(xv0, GroupParams{vz64[gi], vs64[gi]}, 2);
+        if (n3) v1 = quantize_code(xv1, GroupParams{vz64[gi], vs64[gi]}, 2);
+      }
+      *reinterpret_cast<uint16_t*>(ck + t * d + c) = (uint16_t)(k0 | (k1 << 8));
+      cv[c * 34 + t] = (uint8_t)v0;
+      cv[(c + 1) * 34 + t] = (uint8_t)v1;
+    }
+  }
+  __syncthreads();
+  // ---- words
+  constexpr int KW = g * 4 * BITS;  // key (and value) code words per block: 256 (2-bit) / 128 (1-bit)
+  uint32_t* okc = B.kcodes + bi * (size_t)G.rec;
+  uint32_t* ovc = B.vcodes + bi * (size_t)G.rec;
+  for (int w = tid; w < KW; w += 256) {
+    {  // key word: token t, channels c0.. (kloc: LSB-first)
+      const int t = w / (4 * BITS), c0 = (w % (4 * BITS)) * (32 / BITS);
+      uint32_t word = 0;
+      if (BITS == 2) {
+        const uint4 q = *reinterpret_cast<const uint4*>(ck + t * d + c0);
+        const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint32_t x = qq[e];
+          x = (x | (x >> 6)) & 0x000F000Fu;
+          x = (x | (x >> 12)) & 0xFFu;
+          word |= x << (8 * e);
+        }
+      } else {
+        const uint4 q0 = *reinterpret_cast<const uint4*>(ck + t * d + c0);
+        const uint4 q1 = *reinterpret_cast<const uint4*>(ck + t * d + c0 + 16);
+        const uint32_t qq[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          uint32_t x = qq[e];
+          x = x | (x >> 7);
+          x = (x | (x >> 14)) & 0xFu;
+          word |= x << (4 * e);
+        }
+      }
+      okc[w] = word;
+    }
+    {  // value word: inverse of vloc (common.cuh), code pairs (odd = 0, 1) per 16-bit load
+      int mt_base, lane;
+      if (BITS == 2) {
+        mt_base = 4 * (w >> 7) + (w & 3);
+        lane = (w >> 2) & 31;
+      } else {
+        mt_base = 2 * (w & 3);
+        lane = w >> 2;
+      }
+      const int gq = lane >> 2, tq = lane & 3;
+      uint32_t word = 0;
+      constexpr int NR = BITS == 2 ? 8 : 16;  // (rh, q) [+ mt step] fields per half word
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int mt = BITS == 2 ? mt_base : mt_base + (r >> 3);
+        const int rh = BITS == 2 ? (r >> 2) : ((r >> 2) & 1);
+        const int q = r & 3;
+        const int c = 16 * mt + 8 * rh + gq;
+        const int t = 16 * (q >> 1) + 8 * (q & 1) + 2 * tq;
+        const uint32_t x = *reinterpret_cast<const uint16_t*>(cv + c * 34 + t);
+        const uint32_t m = BITS == 2 ? 3u : 1u;
+        word |= ((x & m) << (BITS * r)) | (((x >> 8) & m) << (16 + BITS * r));
+      }
+      ovc[w] = word;
+    }
+  }
+}
+
 size_t quantize_smem_bytes(const Geo& G) {
   size_t s = 2 * sizeof(float) * G.g * G.d;
   s += sizeof(uint32_t) * (2 * (G.g / G.tb) * G.bwords);
@@ -341,8 +549,17 @@ void launch_quantize(const Geo& G, const LayerBufs& B, const QuantSrc& S, int bl
   cudaFuncSetAttribute(k_quantize, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   dim3 grid(nblocks, G.H, G.batch);
   if (G.fast && G.d == 128 && G.g == 32 && (G.bits == 1 || G.bits == 2)) {
-    if (G.bits == 2) k_quantize_fast<2><<<grid, 256, 0, st>>>(G, B, S, blk0);
-    else k_quantize_fast<1><<<grid, 256, 0, st>>>(G, B, S, blk0);
+    static const bool v1 = [] {  // SPC_K1_V1=1: the round-1 kernel (A/B)
+      const char* e = getenv("SPC_K1_V1");
+      return e && atoi(e) != 0;
+    }();
+    if (v1) {
+      if (G.bits == 2) k_quantize_fast<2><<<grid, 256, 0, st>>>(G, B, S, blk0);
+      else k_quantize_fast<1><<<grid, 256, 0, st>>>(G, B, S, blk0);
+    } else {
+      if (G.bits == 2) k_quantize_fast2<2><<<grid, 256, 0, st>>>(G, B, S, blk0);
+      else k_quantize_fast2<1><<<grid, 256, 0, st>>>(G, B, S, blk0);
+    }
     return;
   }
   k_quantize<<<grid, 256, quantize_smem_bytes(G), st>>>(G, B, S, blk0);
