@@ -365,7 +365,7 @@ static void launch_pf(int64_t inflight, int units, const Geo& G, const LayerBufs
     const int ctas = (int)(per / cta2 < 16 ? per / cta2 : 16);
     k_prefetch<2><<<dim3(ctas, one ? 1 : units), kSideThreads, 0, st>>>(G, B, hk, hv, seq, unit, one);
   } else {
-    k_prefetch<4><<<dim3(1, one ? 1 : units), kSideThreads, 0, st>>>(G, B, hk, hv, seq, unit, one);
+    k_prefetch<1><<<dim3(1, one ? 1 : units), kSideThreads, 0, st>>>(G, B, hk, hv, seq, unit, one);
   }
 }
 

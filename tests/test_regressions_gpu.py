@@ -104,3 +104,39 @@ def test_adapter_decodes_past_max_len():
     budget = CacheBudget(bits=2, group_size=8, residual=8, prefetch_k=8, context_length=48)
     res = generate(cfg, w, prompt, 20, budget, ChannelModel(bandwidth=1e6))   # 40 + 20 > 48
     assert len(res.tokens) == 21
+
+
+def test_debug_and_measurement_entry_points():
+    """Round-2 C ABI additions: the fp32 debug output (off -> ValueError), the
+    prefetch wall-time union and the host-link peak probe."""
+    import ctypes
+
+    import torch
+    from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache, SpeculativeLayerDecoder, _lib
+    rng = np.random.default_rng(8)
+    K, V = make_kv(rng, 600, 2, 128)
+    cache = DeviceTwoTierCache(1, 2, 128, CacheBudget(bits=2, group_size=32, residual=64, prefetch_k=32,
+                                                      context_length=640), q_heads=8)
+    cache.prefill(0, K[None], V[None])
+    dec = SpeculativeLayerDecoder(cache)
+    with pytest.raises(ValueError):
+        dec.debug_out_f32(0, 1)                    # not enabled
+    dec.debug_output_f32(True)
+    q = make_queries(rng, 1, 8, 128)
+    kn, vn = make_step_kv(rng, 1, 2, 128)
+    out = dec.predecode_layer(0, q[None], kn[None], vn[None])
+    o32 = dec.debug_out_f32(0, 1)
+    assert torch.equal(out.float(), o32.to(torch.bfloat16).float())
+    cache.profile(True)
+    q2 = make_queries(rng, 2, 8, 128)
+    kn, vn = make_step_kv(rng, 2, 2, 128)
+    dec.decode_layer(0, 1, q2[None], kn[None], vn[None])
+    prof = cache.profile(False)
+    wall = _lib.lib().spc_profile_prefetch_wall_ms(cache.handle)
+    assert 0.0 <= wall <= prof["prefetch_ms"] + 1e-6
+    cache.close()
+    dma, zc = ctypes.c_double(), ctypes.c_double()
+    _lib.check(_lib.lib().spc_h2d_peak(0, 64 << 20, ctypes.byref(dma), ctypes.byref(zc)))
+    assert 1.0 < dma.value < 200.0 and 1.0 < zc.value < 200.0
+    with pytest.raises(ValueError):
+        _lib.check(_lib.lib().spc_h2d_peak(0, 1000, ctypes.byref(dma), ctypes.byref(zc)))
