@@ -541,6 +541,8 @@ def run_gpu_arm(args, cfg):
                                host_layers=host_layers)
     if args.pf_inflight:
         cache.set_prefetch_inflight(args.pf_inflight)
+    if args.agg_mode != "spill":
+        cache.set_agg_mode(args.agg_mode)
     reduce_layer = None
     if reduce_agg:
         from paper_2503_16163_b200.shard import allreduce_sum
@@ -723,7 +725,7 @@ def run_gpu_arm(args, cfg):
         "config": workload_config(gcfg, world, args, part),
         "rank_share": {"kv_heads": cfg["kv_heads"], "q_heads": cfg["q_heads"], "batch": cfg["batch"],
                        "host_layers": host_layers, "attention_impl": "fast" if cache.fast_path else "generic",
-                       "prefetch_inflight_bytes": args.pf_inflight or None,
+                       "prefetch_inflight_bytes": args.pf_inflight or None, "agg_mode": args.agg_mode,
                        "host_slabs_note": "layers l, l' with l = l' mod host_layers share one pinned slow-tier "
                                           "slab and are fed identical KV (host RAM); PCIe bytes unchanged"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -973,6 +975,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--host-layers", type=int, default=0)
+    ap.add_argument("--agg-mode", default="spill", choices=["spill", "recompute"],
+                    help="top-k aggregate: spill the speculative logits (default) or recompute them (K3r)")
     ap.add_argument("--compute-priority", type=int, default=0,
                     help="CUDA stream priority of the decode loop (negative = higher; 0 = default stream priority)")
     ap.add_argument("--pf-inflight", type=int, default=0,

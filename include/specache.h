@@ -143,6 +143,12 @@ SPC_API int spc_debug_agg(spc_cache* cache, int layer, float* agg, void* stream)
  * attention output in fp32 before the bf16 rounding (the north star's tolerance
  * applies to the fp32-accumulated result; bf16 I/O adds one RN rounding). */
 SPC_API int spc_debug_output_f32(spc_cache* cache, int enable);
+/* The speculative-row aggregate of the top-k (engine.py:317; SURVEY hard part
+ * (b)): 0 = spill (default: the attention kernel writes the speculative rows'
+ * log2 logits, K3b normalises and sums them), 1 = recompute (no spill of
+ * packed positions; K3r re-reads the key codes and recomputes the scores).
+ * The fast path only; the exact kernel always spills. */
+SPC_API int spc_set_agg_mode(spc_cache* cache, int mode);
 /* Wall time (ms) of the K5 prefetch kernels of the last profiled window: the
  * union of their intervals on the two copy streams. */
 SPC_API double spc_profile_prefetch_wall_ms(const spc_cache* cache);

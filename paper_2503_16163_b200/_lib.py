@@ -50,6 +50,7 @@ _SIGS = {
     "spc_ticket": (_I, [_P, _I, _P, _P, _P]),
     "spc_debug_agg": (_I, [_P, _I, _P, _P]),
     "spc_debug_output_f32": (_I, [_P, _I]),
+    "spc_set_agg_mode": (_I, [_P, _I]),
     "spc_profile_prefetch_wall_ms": (ctypes.c_double, [_P]),
     "spc_h2d_peak": (_I, [_I, _I64, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "spc_debug_out_f32": (_I, [_P, _I, _P, _P]),

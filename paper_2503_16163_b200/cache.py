@@ -113,6 +113,12 @@ class DeviceTwoTierCache:
         """'auto' | 'generic' (exact float64 dequant) | 'fast' (tensor cores)."""
         _lib.check(_lib.lib().spc_set_attend_impl(self._h, {"auto": 0, "generic": 1, "fast": 2}[impl]))
 
+    def set_agg_mode(self, mode: str) -> None:
+        """Top-k aggregate: 'spill' (default) or 'recompute' (SURVEY hard part (b))."""
+        if mode not in ("spill", "recompute"):
+            raise ValueError("agg mode must be 'spill' or 'recompute'")
+        _lib.check(_lib.lib().spc_set_agg_mode(self._h, 0 if mode == "spill" else 1))
+
     def set_prefetch_inflight(self, nbytes: int) -> None:
         """K5 sysmem bytes in flight over the batch (0 = default 256 KiB)."""
         _lib.check(_lib.lib().spc_set_prefetch_inflight(self._h, int(nbytes)))

@@ -76,6 +76,7 @@ struct spc_cache {
   Geo G{};
   int device = 0;
   int impl = 0;  // 0 auto, 1 generic exact, 2 fast
+  int agg_mode = 0;  // 0 spill (K2 writes the speculative logits), 1 recompute (K3r)
   int64_t pf_inflight = int64_t(256) << 10;  // K5 sysmem bytes in flight (spc_set_prefetch_inflight)
   std::vector<LayerBufs> L;
   std::vector<void*> dev_allocs;
@@ -236,6 +237,7 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
   a.sm_scale_log2 = (float)(1.0 / std::sqrt((double)G.d) * 1.4426950408889634);
   a.out_f32 = c->dbg_out ? c->dbg_out + (size_t)layer * G.batch * 2 * G.Hq * G.d : nullptr;
   bool fast = (c->impl != 1) && attend_fast_supported(G, rows);
+  a.agg_recompute = (c->agg_mode == 1 && fast) ? 1 : 0;
   if (c->impl == 2 && !fast) return fail(SPC_EINVAL, "fast attention path not available for this geometry");
   cudaEvent_t p0 = nullptr, p1 = nullptr;
   if (c->prof) {
@@ -272,7 +274,10 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
     p0 = prof_event(c);
     CUDA_TRY(cudaEventRecord(p0, cs));
   }
-  if (!(debug_skip() & 1)) launch_agg(a, cs);
+  if (!(debug_skip() & 1)) {
+    if (a.agg_recompute) launch_agg_recompute(a, cs);
+    else launch_agg(a, cs);
+  }
   c->launches += a.f > 0;
   CUDA_TRY(cudaGetLastError());
   if (c->agg_ext) {  // the caller reduces agg across ranks on cs, then spc_finish_layer
@@ -537,6 +542,12 @@ int64_t spc_row_bytes(const spc_cache* c, int64_t positions) {
 int spc_set_attend_impl(spc_cache* c, int impl) {
   if (!c || impl < 0 || impl > 2) return fail(SPC_EINVAL, "impl must be 0 (auto), 1 (generic) or 2 (fast)");
   c->impl = impl;
+  return SPC_OK;
+}
+
+int spc_set_agg_mode(spc_cache* c, int mode) {
+  if (!c || mode < 0 || mode > 1) return fail(SPC_EINVAL, "agg mode must be 0 (spill) or 1 (recompute)");
+  c->agg_mode = mode;
   return SPC_OK;
 }
 

@@ -130,4 +130,102 @@ void launch_agg(const AttnArgs& a, cudaStream_t st) {
   k_agg<<<dim3(blocks, a.G.U, a.G.batch), kSideThreads, 2 * heads * sizeof(float), st>>>(a);
 }
 
+// K3r (spc_set_agg_mode(cache, 1), SURVEY hard part (b) option 2): the
+// aggregate without the spill.  K2 writes no packed-position logits; this
+// kernel re-reads each 32-token record's key codes and key params and
+// recomputes the speculative row's log2 scores of the unit's q heads on the
+// CUDA cores (fp32, dequantized keys like materialize, kvcache.py:222-243),
+// then agg[i] = sum_h exp2(s_h[i] - M_h) / Z_h with the combined (M, Z).
+// Pinned positions keep the exact-row logits the exact segment spilled.  The
+// measured point of this option: it streams the key half of the packed tier
+// again (48 B / 32 B per token per KV head at 2 / 1 bit) against the spill's
+// 8 B / 32 B write + read.
+constexpr int kAggRcWarps = 8;
+__global__ void __launch_bounds__(kAggRcWarps * 32) k_agg_recompute(AttnArgs a) {
+  const Geo G = a.G;
+  const int u = blockIdx.y, b = blockIdx.z, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kh0 = G.scope ? u : 0, nkv = G.scope ? 1 : G.H, nq = nkv * G.G, j0 = kh0 * G.G;
+  extern __shared__ float sm[];
+  float* sQ = sm;                      // [nq][d] speculative-row queries * d^-0.5 * log2(e)
+  float* sM = sQ + nq * G.d;           // [nq]
+  float* sI = sM + nq;                 // [nq]
+  float* sP = sI + nq;                 // [warps][2][d] key params (s, z) of the warp's current head
+  float* sAcc = sP + kAggRcWarps * 2 * G.d;  // [warps][32]
+  for (int x = threadIdx.x; x < nq * G.d; x += blockDim.x) {
+    const int j = x / G.d, c = x - j * G.d;
+    sQ[x] = __bfloat162float(a.q[(((size_t)b * a.rows + a.agg_row) * G.Hq + j0 + j) * G.d + c]) * a.sm_scale_log2;
+  }
+  for (int x = threadIdx.x; x < nq; x += blockDim.x) {
+    sM[x] = a.mz[((size_t)b * G.Hq + j0 + x) * 2];
+    sI[x] = 1.f / a.mz[((size_t)b * G.Hq + j0 + x) * 2 + 1];
+  }
+  __syncthreads();
+  const int nblk = a.f / G.tb;
+  const uint32_t* bm = a.B.bitmap + ((size_t)b * G.U + u) * (G.L / 32);
+  const uint32_t mask = (1u << G.bits) - 1u;
+  float* wp = sP + warp * 2 * G.d;
+  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int t = lane, pos = blk * G.tb + t;
+    const bool pinned = (bm[pos >> 5] >> (pos & 31)) & 1u;
+    float acc = 0.f;
+    for (int kq = warp; kq < nkv; kq += kAggRcWarps) {
+      const int kh = kh0 + kq;
+      const size_t bi = blk_index(G, b, kh, blk);
+      const uint32_t* rec = a.B.kcodes + bi * (size_t)G.rec;
+      const uint32_t* kp = a.B.kparams + bi * (size_t)G.rec;
+      __syncwarp();
+      for (int c = lane; c < G.d; c += 32) {  // group params of this record, per channel
+        const GroupParams p = params_from_word(kp[kpi(G, c)], G.bits);
+        wp[c] = (float)p.scale;
+        wp[G.d + c] = (float)p.zero;
+      }
+      __syncwarp();
+      float dot[8];
+#pragma unroll
+      for (int g2 = 0; g2 < 8; ++g2) dot[g2] = 0.f;
+      const uint32_t* row = rec + t * G.krw;  // token t's key codes, channels LSB-first (kloc)
+      for (int w = 0; w < G.krw; ++w) {
+        const uint32_t word = row[w];
+        const int per = 32 / G.bits;
+#pragma unroll 4
+        for (int e = 0; e < per; ++e) {
+          const int c = w * per + e;
+          if (c >= G.d) break;
+          const float kv = fmaf((float)((word >> (G.bits * e)) & mask), wp[c], wp[G.d + c]);
+#pragma unroll
+          for (int g2 = 0; g2 < 8; ++g2)
+            if (g2 < G.G) dot[g2] = fmaf(kv, sQ[(kq * G.G + g2) * G.d + c], dot[g2]);
+        }
+      }
+#pragma unroll
+      for (int g2 = 0; g2 < 8; ++g2) {
+        if (g2 >= G.G) break;
+        const int jl = kq * G.G + g2;
+        const float s2 = pinned ? a.spill[((size_t)b * G.Hq + j0 + jl) * G.L + pos] : dot[g2];
+        acc += exp2f(s2 - sM[jl]) * sI[jl];
+      }
+    }
+    sAcc[warp * 32 + lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+      float tot = 0.f;
+#pragma unroll
+      for (int w2 = 0; w2 < kAggRcWarps; ++w2) tot += sAcc[w2 * 32 + lane];
+      a.B.agg[((size_t)b * G.U + u) * G.L + pos] = tot;
+    }
+    __syncthreads();
+  }
+}
+
+void launch_agg_recompute(const AttnArgs& a, cudaStream_t st) {
+  if (a.f <= 0) return;
+  const Geo& G = a.G;
+  const int nq = (G.scope ? 1 : G.H) * G.G;
+  const size_t smem = sizeof(float) * ((size_t)nq * G.d + 2 * nq + kAggRcWarps * 2 * G.d + kAggRcWarps * 32);
+  cudaFuncSetAttribute(k_agg_recompute, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int nblk = a.f / G.tb;
+  const int blocks = std::min(nblk, std::max(1, 2 * 148 * 4 / (G.U * G.batch)));
+  k_agg_recompute<<<dim3(blocks, G.U, G.batch), kAggRcWarps * 32, smem, st>>>(a);
+}
+
 }  // namespace spc

@@ -958,7 +958,7 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
 #pragma unroll
   for (int e = 0; e < RPL; ++e) {
     jr[e] = PACK ? tq : 2 * tq + e;
-    spr[e] = (jr[e] < NR && jr[e] >= agg_j0 && jr[e] < agg_j0 + G.G)
+    spr[e] = (!a.agg_recompute && jr[e] < NR && jr[e] >= agg_j0 && jr[e] < agg_j0 + G.G)
                  ? a.spill + ((size_t)b * G.Hq + h * G.G + (jr[e] - agg_j0)) * G.L : nullptr;
   }
 

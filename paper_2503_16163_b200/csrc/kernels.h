@@ -34,6 +34,7 @@ struct AttnArgs {
   float* mz;                   // [b][Hq][2] agg-row (max, sum), log2 domain
   float sm_scale_log2;         // d^-0.5 * log2(e)
   float* out_f32;              // debug (spc_debug_output_f32): the combine's fp32 O before bf16 rounding
+  int agg_recompute;           // 1: K2 spills no packed-position logits; K3r recomputes them (spc_set_agg_mode)
 };
 
 size_t quantize_smem_bytes(const Geo& G);
@@ -52,6 +53,7 @@ int attend_fast_supported(const Geo& G, int rows);
 int launch_attend_fast(const AttnArgs& a, cudaStream_t st);  // returns kernels launched
 void launch_combine(const AttnArgs& a, cudaStream_t st);
 void launch_agg(const AttnArgs& a, cudaStream_t st);
+void launch_agg_recompute(const AttnArgs& a, cudaStream_t st);
 
 // K4 select + pin diff, K5 prefetch gather (zero-copy from pinned host), K6 append
 void launch_topk(const Geo& G, const LayerBufs& B, int f, cudaStream_t st);

@@ -109,7 +109,7 @@ def test_decode_layer_matches_reference_run(tag, impl):
     cache.close()
 
 
-def _oracle_run(cfg, seed, steps=3, impl="auto"):
+def _oracle_run(cfg, seed, steps=3, impl="auto", agg_mode="spill"):
     """Seeded C1-like run: device vs oracle for predecode + `steps` decode steps."""
     import torch
     from paper_2503_16163_b200 import CacheBudget, DeviceTwoTierCache
@@ -125,6 +125,7 @@ def _oracle_run(cfg, seed, steps=3, impl="auto"):
     budget = CacheBudget(bits=bits, group_size=g, residual=r, prefetch_k=k, context_length=n0 + steps + 8)
     cache = DeviceTwoTierCache(1, H, d, budget, batch=b, q_heads=Hq, topk_scope=scope)
     cache.set_attend_impl(impl)
+    cache.set_agg_mode(agg_mode)
     cache.prefill(0, np.stack([x[0] for x in KV]), np.stack([x[1] for x in KV]))
     dec = _dec(cache)
     dec.debug_output_f32(True)
@@ -152,9 +153,13 @@ def _oracle_run(cfg, seed, steps=3, impl="auto"):
         outs32 = dec.debug_out_f32(0, 2).cpu().numpy()
         pm = res.pinned_mass.cpu().numpy()
         picked, newc = dec.ticket(0)
+        aggs = dec.debug_agg(0).cpu().numpy()
         for s in range(b):
+            f_s = states[s].f
             o = R.decode_layer(states[s], qcur[s], kn[s], vn[s])
             assert_out_close(outs[s], o["out"], outs32[s])
+            for u in range(U):
+                np.testing.assert_allclose(aggs[s, u, :f_s], o["agg"][u][:f_s], rtol=1e-4, atol=1e-7)
             np.testing.assert_allclose(pm[s], o["pinned_mass"], rtol=1e-4, atol=1e-6)
             for u in range(U):
                 got = [p for p in picked[s, u].tolist() if p >= 0]
@@ -171,6 +176,16 @@ def _oracle_run(cfg, seed, steps=3, impl="auto"):
 def test_c1_geometry_vs_oracle(impl):
     # BASELINE config 1: 32 heads x d=128, ctx 4096, 2-bit, k=64, r=32, batch 1
     _oracle_run((1, 4096, 32, 32, 128, 2, 32, 32, 64, "layer"), seed=11, impl=impl)
+
+
+@pytest.mark.parametrize("cfg", [(1, 4096, 32, 32, 128, 2, 32, 32, 64, "layer"),
+                                 (3, 1500, 2, 8, 128, 1, 32, 64, 32, "layer"),
+                                 (2, 1200, 4, 16, 128, 1, 32, 64, 16, "kv_head")])
+def test_agg_recompute_vs_oracle(cfg):
+    """SURVEY hard part (b) option 2 (spc_set_agg_mode 'recompute'): no spill of
+    packed-position logits, the aggregate recomputed from the key codes -- the
+    aggregate, top-k, outputs and pinned mass must match the oracle as with the spill."""
+    _oracle_run(cfg, seed=17, agg_mode="recompute")
 
 
 @pytest.mark.parametrize("bits", [1, 2])
