@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(kCH) k_attend_generic(AttnArgs a) {
 void launch_attend_generic(const AttnArgs& a, cudaStream_t st) {
   const Geo& G = a.G;
   size_t smem = generic_smem_bytes(G, a.rows);
-  cudaFuncSetAttribute(k_attend_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);  // per device
+  static std::atomic<unsigned long long> done{0};
+  ensure_smem_attr(done, k_attend_generic, 200 * 1024);
   dim3 grid(a.nsplit + 1, G.H, G.batch);
   k_attend_generic<<<grid, kCH, smem, st>>>(a);
 }

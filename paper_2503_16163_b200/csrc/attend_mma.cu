@@ -1667,7 +1667,8 @@ void launch_fast_t(const AttnArgs& a, cudaStream_t st) {
   constexpr size_t smem = fast_smem_bytes<BITS, NR>();
   // two CTAs per SM (228 KB, 1 KB reserved per CTA) is the design point
   static_assert(smem * kMinBlocks <= 227 * 1024, "K2 shared memory exceeds kMinBlocks CTAs/SM");
-  cudaFuncSetAttribute(k_attend_fast<BITS, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  // per device
+  static std::atomic<unsigned long long> done{0};  // one per <BITS, NR> instantiation
+  ensure_smem_attr(done, k_attend_fast<BITS, NR>, (int)smem);
   dim3 grid = kExactOrder == 0 ? dim3(a.nsplit + 1, a.G.H, a.G.batch)
                                 : dim3((a.nsplit + 1) * a.G.H * a.G.batch);
   k_attend_fast<BITS, NR><<<grid, kThreads, smem, st>>>(a);

@@ -29,6 +29,8 @@
 // (quant.py:59-73) is reconstructed bit-exactly on device; the normative fp16
 // (zero, scale) is a direct float64->fp16 rounding of those (quant.py:150-160).
 #pragma once
+#include <atomic>
+#include <cuda_runtime.h>
 // Threads per CTA of the side kernels that run beside K2 on the copy and
 // selection streams (K3b aggregate, K5 PCIe gather).  128 with <= 32 registers
 // fits in the 4096 registers two 120-register K2 CTAs leave free on an SM
@@ -42,6 +44,19 @@
 #include <stdint.h>
 
 namespace spc {
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device), thread
+// safe: the attribute is per device, so a process-wide "done" flag would skip
+// the second device (round-1 advisor finding), and setting it on every launch
+// costs a driver call on the launch path.  `done` is the kernel's own bit mask.
+template <typename F>
+inline void ensure_smem_attr(std::atomic<unsigned long long>& done, F* kernel, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
 constexpr int kSideThreads = SPC_SIDE_THREADS;
 // launch-bound occupancy hint that caps the side kernels at 32 registers when narrow
 constexpr int kSideMinBlocks = kSideThreads <= 128 ? 16 : 1;

@@ -544,9 +544,8 @@ size_t quantize_smem_bytes(const Geo& G) {
 void launch_quantize(const Geo& G, const LayerBufs& B, const QuantSrc& S, int blk0, int nblocks,
                      cudaStream_t st) {
   if (nblocks <= 0) return;
-  // set on every launch: the attribute is per device, and a process-wide flag
-  // would skip the second device of a multi-device process
-  cudaFuncSetAttribute(k_quantize, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  static std::atomic<unsigned long long> done{0};
+  ensure_smem_attr(done, k_quantize, 200 * 1024);
   dim3 grid(nblocks, G.H, G.batch);
   if (G.fast && G.d == 128 && G.g == 32 && (G.bits == 1 || G.bits == 2)) {
     static const bool v1 = [] {  // SPC_K1_V1=1: the round-1 kernel (A/B)
