@@ -43,53 +43,78 @@ void launch_attend_generic(const AttnArgs& a, cudaStream_t st) {
 
 // ---------------------------------------------------------------------------------
 // K3a: merge split partials -> O (bf16), agg-row (max, sum), pinned mass.
-__global__ void k_combine(AttnArgs a) {
+// One CTA per (q head, seq, row).  Warp 0 reduces the row's per-split (max,
+// sum) with lanes striding the splits and leaves one factor exp2(m_s - M) per
+// split in shared memory; every thread then sums its channel over the splits,
+// eight independent loads at a time.  The kernel sits on the compute stream
+// between two attention launches and is memory-latency bound (ncu: 87%
+// long-scoreboard stalls, 11% warps active in round 1's one-CTA-per-head form).
+constexpr int kCombineSplits = 132;  // >= kSplitCap + 1 (api.cu) + padding
+__global__ void __launch_bounds__(128) k_combine(AttnArgs a) {
   const Geo G = a.G;
-  const int hq = blockIdx.x, b = blockIdx.y, h = hq / G.G, gq = hq - h * G.G;
-  const int R = a.rows * G.G, S = a.nsplit + 1;
-  for (int r = 0; r < a.rows; ++r) {
-    const int j = r * G.G + gq;
-    const size_t base = ((size_t)b * G.H + h) * S * R;
+  const int hq = blockIdx.x, b = blockIdx.y, r = blockIdx.z, h = hq / G.G, gq = hq - h * G.G;
+  const int R = a.rows * G.G, S = a.nsplit + 1, j = r * G.G + gq;
+  const int lane = threadIdx.x & 31;
+  __shared__ float sf[kCombineSplits];
+  __shared__ float sML[2];
+  const size_t base = ((size_t)b * G.H + h) * S * R;
+  if (threadIdx.x < 32) {
     float M = -CUDART_INF_F;
-    for (int s = 0; s < S; ++s) {
-      float l = a.part_ml[(base + (size_t)s * R + j) * 2 + 1];
-      if (l > 0.f) M = fmaxf(M, a.part_ml[(base + (size_t)s * R + j) * 2]);
+    for (int s = lane; s < S; s += 32) {
+      const float2 ml = *reinterpret_cast<const float2*>(&a.part_ml[(base + (size_t)s * R + j) * 2]);
+      if (ml.y > 0.f) M = fmaxf(M, ml.x);
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float L = 0.f;
-    for (int s = 0; s < S; ++s) {
-      float l = a.part_ml[(base + (size_t)s * R + j) * 2 + 1];
-      if (l > 0.f) L += l * exp2f(a.part_ml[(base + (size_t)s * R + j) * 2] - M);
+    for (int s = lane; s < S; s += 32) {
+      const float2 ml = *reinterpret_cast<const float2*>(&a.part_ml[(base + (size_t)s * R + j) * 2]);
+      const float f = ml.y > 0.f ? exp2f(ml.x - M) : 0.f;
+      sf[s] = f;
+      L = fmaf(ml.y, f, L);
     }
-    const float invL = 1.f / L;
-    for (int c = threadIdx.x; c < G.d; c += blockDim.x) {
-      float o = 0.f;
-      for (int s = 0; s < S; ++s) {
-        float l = a.part_ml[(base + (size_t)s * R + j) * 2 + 1];
-        if (l > 0.f)
-          o = fmaf(a.part_o[(base + (size_t)s * R + j) * G.d + c],
-                   exp2f(a.part_ml[(base + (size_t)s * R + j) * 2] - M), o);
-      }
-      const size_t oi = (((size_t)b * a.rows + r) * G.Hq + hq) * G.d + c;
-      a.out[oi] = __float2bfloat16_rn(o * invL);
-      if (a.out_f32) a.out_f32[oi] = o * invL;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (lane == 0) {
+      sML[0] = M;
+      sML[1] = L;
     }
-    if (threadIdx.x == 0) {
-      if (r == a.agg_row) {
-        a.mz[((size_t)b * G.Hq + hq) * 2 + 0] = M;
-        a.mz[((size_t)b * G.Hq + hq) * 2 + 1] = L;
-      }
-      if (r == 0 && a.pinned_mass) {
-        size_t pb = ((size_t)b * G.H + h) * R + j;
-        float pl = a.pin_ml[pb * 2 + 1];
-        a.pinned_mass[(size_t)b * G.Hq + hq] =
-            pl > 0.f ? pl * exp2f(a.pin_ml[pb * 2] - M) * invL : 0.f;
-      }
+  }
+  __syncthreads();
+  const float M = sML[0], L = sML[1], invL = 1.f / L;
+  const size_t sstride = (size_t)R * G.d;
+  for (int c = threadIdx.x; c < G.d; c += blockDim.x) {
+    const float* po = a.part_o + (base + j) * G.d + c;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int s0 = 0;
+    for (; s0 + 8 <= S; s0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = po[(size_t)(s0 + u) * sstride];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = fmaf(v[u], sf[s0 + u], acc[u]);
+    }
+    for (int s = s0; s < S; ++s) acc[0] = fmaf(po[(size_t)s * sstride], sf[s], acc[0]);
+    const float o = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    const size_t oi = (((size_t)b * a.rows + r) * G.Hq + hq) * G.d + c;
+    a.out[oi] = __float2bfloat16_rn(o * invL);
+    if (a.out_f32) a.out_f32[oi] = o * invL;
+  }
+  if (threadIdx.x == 0) {
+    if (r == a.agg_row) {
+      a.mz[((size_t)b * G.Hq + hq) * 2 + 0] = M;
+      a.mz[((size_t)b * G.Hq + hq) * 2 + 1] = L;
+    }
+    if (r == 0 && a.pinned_mass) {
+      size_t pb = ((size_t)b * G.H + h) * R + j;
+      float pl = a.pin_ml[pb * 2 + 1];
+      a.pinned_mass[(size_t)b * G.Hq + hq] = pl > 0.f ? pl * exp2f(a.pin_ml[pb * 2] - M) * invL : 0.f;
     }
   }
 }
 
 void launch_combine(const AttnArgs& a, cudaStream_t st) {
-  k_combine<<<dim3(a.G.Hq, a.G.batch), 128, 0, st>>>(a);
+  k_combine<<<dim3(a.G.Hq, a.G.batch, a.rows), 128, 0, st>>>(a);
 }
 
 // K3b: agg[i] = sum over the unit's q heads of A_j[agg_row, i], i < f, in
