@@ -58,6 +58,15 @@ __global__ void __launch_bounds__(128) k_combine(AttnArgs a) {
   __shared__ float sf[kCombineSplits];
   __shared__ float sML[2];
   const size_t base = ((size_t)b * G.H + h) * S * R;
+  // the first 16 splits' partials are loaded before the barrier: they do not
+  // depend on the factors, so their latency overlaps warp 0's (max, sum) pass
+  const size_t sstride = (size_t)R * G.d;
+  const int c0 = threadIdx.x;
+  const bool cl = c0 < G.d;
+  const float* po = a.part_o + (base + j) * G.d + (cl ? c0 : 0);
+  float pre[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) pre[u] = (cl && u < S) ? po[(size_t)u * sstride] : 0.f;
   if (threadIdx.x < 32) {
     float M = -CUDART_INF_F;
     for (int s = lane; s < S; s += 32) {
@@ -82,19 +91,24 @@ __global__ void __launch_bounds__(128) k_combine(AttnArgs a) {
   }
   __syncthreads();
   const float M = sML[0], L = sML[1], invL = 1.f / L;
-  const size_t sstride = (size_t)R * G.d;
-  for (int c = threadIdx.x; c < G.d; c += blockDim.x) {
-    const float* po = a.part_o + (base + j) * G.d + c;
+  for (int c = c0; c < G.d; c += blockDim.x) {
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     int s0 = 0;
+    if (c == c0) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (u < S) acc[u & 7] = fmaf(pre[u], sf[u], acc[u & 7]);
+      s0 = 16;
+    }
+    const float* pc = a.part_o + (base + j) * G.d + c;
     for (; s0 + 8 <= S; s0 += 8) {
       float v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = po[(size_t)(s0 + u) * sstride];
+      for (int u = 0; u < 8; ++u) v[u] = pc[(size_t)(s0 + u) * sstride];
 #pragma unroll
       for (int u = 0; u < 8; ++u) acc[u] = fmaf(v[u], sf[s0 + u], acc[u]);
     }
-    for (int s = s0; s < S; ++s) acc[0] = fmaf(po[(size_t)s * sstride], sf[s], acc[0]);
+    for (int s = s0; s < S; ++s) acc[0] = fmaf(pc[(size_t)s * sstride], sf[s], acc[0]);
     const float o = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     const size_t oi = (((size_t)b * a.rows + r) * G.Hq + hq) * G.d + c;
     a.out[oi] = __float2bfloat16_rn(o * invL);
