@@ -238,6 +238,9 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
   a.out_f32 = c->dbg_out ? c->dbg_out + (size_t)layer * G.batch * 2 * G.Hq * G.d : nullptr;
   bool fast = (c->impl != 1) && attend_fast_supported(G, rows);
   a.agg_recompute = (c->agg_mode == 1 && fast) ? 1 : 0;
+  // K6a (row 0 -> residual ring) rides on the combine kernel when the rows are
+  // 16-byte vectors (they are: run_layer requires 16-byte aligned inputs)
+  a.ring_append = (append_row0 && G.d % 8 == 0) ? 1 : 0;
   if (c->impl == 2 && !fast) return fail(SPC_EINVAL, "fast attention path not available for this geometry");
   cudaEvent_t p0 = nullptr, p1 = nullptr;
   if (c->prof) {
@@ -260,7 +263,7 @@ int run_layer(spc_cache* c, int layer, int rows, const void* q, const void* k_ne
     c->prof_attn.push_back({p0, p1});
   }
   const int n_before = (int)c->n[layer];
-  if (append_row0) {  // K6a on the compute stream (reads the caller's k_new/v_new now)
+  if (append_row0 && !a.ring_append) {  // K6a on the compute stream (reads the caller's k_new/v_new now)
     launch_ring_append(G, c->L[layer], (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new,
                        (long long)rows * G.H * G.d, n_before, st);
     c->launches += 1;

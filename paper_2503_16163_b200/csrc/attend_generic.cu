@@ -114,6 +114,16 @@ __global__ void __launch_bounds__(128) k_combine(AttnArgs a) {
     a.out[oi] = __float2bfloat16_rn(o * invL);
     if (a.out_f32) a.out_f32[oi] = o * invL;
   }
+  if (a.ring_append && r == 0 && gq == 0) {
+    // K6a fused: row 0's K and V of kv head h into the residual ring, slot n % ring
+    // (kvcache.py:162-171; the attention of this layer has finished reading the ring)
+    const size_t ro = (((size_t)b * G.H + h) * G.ring + a.n % G.ring) * G.d;
+    const size_t io = ((size_t)b * a.rows * G.H + h) * G.d;
+    for (int x = threadIdx.x * 8; x < G.d; x += blockDim.x * 8) {
+      *reinterpret_cast<uint4*>(a.B.ring_k + ro + x) = *reinterpret_cast<const uint4*>(a.k_new + io + x);
+      *reinterpret_cast<uint4*>(a.B.ring_v + ro + x) = *reinterpret_cast<const uint4*>(a.v_new + io + x);
+    }
+  }
   if (threadIdx.x == 0) {
     if (r == a.agg_row) {
       a.mz[((size_t)b * G.Hq + hq) * 2 + 0] = M;

@@ -35,6 +35,7 @@ struct AttnArgs {
   float sm_scale_log2;         // d^-0.5 * log2(e)
   float* out_f32;              // debug (spc_debug_output_f32): the combine's fp32 O before bf16 rounding
   int agg_recompute;           // 1: K2 spills no packed-position logits; K3r recomputes them (spc_set_agg_mode)
+  int ring_append;             // 1: the combine also writes row 0's K/V into the residual ring (K6a fused)
 };
 
 size_t quantize_smem_bytes(const Geo& G);
