@@ -1693,8 +1693,7 @@ int launch_attend_fast(const AttnArgs& a0, cudaStream_t st) {
   // splits plus one exact CTA per unit) of b blocks costs about ceil(C / slots)
   // rounds of (b + c0) block-times, c0 ~ 20 blocks covering a CTA's prologue
   // (ring fill, first DRAM round trip) and merge.  Short CTAs pay c0 too often,
-  // few CTAs quantize badly.  Measured sweep (SPC_NSPLIT): the
-  // model's picks C2 5, C3 16, C4 16 are within 1.3% of the best split.
+  // few CTAs quantize badly.  Measured sweeps (SPC_NSPLIT).
   static const int waves = [] {
     const char* e = getenv("SPC_SPLIT_WAVES");
     return e ? std::max(1, atoi(e)) : 0;
@@ -1722,7 +1721,11 @@ int launch_attend_fast(const AttnArgs& a0, cudaStream_t st) {
     for (int w = 1; w <= cap; ++w) {
       const int bps = std::max(1, (nblk + w - 1) / w), ns = std::max(1, (nblk + bps - 1) / bps);
       const long long rounds = ((long long)units * (ns + 1) + slots - 1) / slots;  // + the exact CTA
-      const long long cost = rounds * (bps + c0);
+      // a launch that needs a second round pays ~bps/10 more in the layer loop (its
+      // later CTAs start behind the side kernels' CTAs): the C4 rank share's single
+      // 8-split wave beats the model's 17-split two rounds by 10% in the bench
+      // (profiles/r2_34_*), while C2 (7) and C3 (22) keep their picks
+      const long long cost = rounds * (bps + c0) + (rounds > 1 ? bps / 10 : 0);
       if (best < 0 || cost < best) {
         best = cost;
         want = w;
