@@ -100,6 +100,31 @@ constexpr bool kHalfKeyB = SPC_K2_HKB != 0;
 // sum_t P * z runs on the tensor cores: one m16n8k16 with A rows 0-3 = z' hi of
 // the four groups, rows 4-7 = z' lo, and B = the P hi / lo fragments.
 constexpr bool kVCoop = SPC_K2_VCOOP != 0;
+#ifndef SPC_K2_FOLD
+#define SPC_K2_FOLD 16
+#endif
+#ifndef SPC_K2_FOLD_PG
+#define SPC_K2_FOLD_PG 16
+#endif
+#ifndef SPC_K2_FOLD_MIN
+#define SPC_K2_FOLD_MIN 32
+#endif
+// Accumulator fold (SPC_K2_FOLD = F; 0 = off): every F blocks a warp adds its
+// z sums (sum_t P z) into the value accumulator and restarts them.  mma.sync's
+// fp32 accumulation truncates each k-step's sum to the accumulator's exponent,
+// a bias toward zero of ~2^-24 |D| per MMA.  With unsigned codes the scale part
+// sum_t P s code and the zero-point part sum_t P z each grow linearly over a
+// warp's blocks while their sum (the output) is a random walk that largely
+// cancels them, so the bias is amplified: measured at the C4 rank share (1 KV
+// head, 128k, 8 splits = 64 blocks per warp) the fp32 output's per-head error
+// was 2.6e-3 and fell as 1/(blocks per warp) with more splits
+// (profiles/r2_35_fold.json).  Folding keeps both accumulators at the output's
+// scale: 2.6e-3 -> 1.9e-4 there (F = 16), for ~50 instructions per F blocks per
+// warp.  Only launches whose warps walk more than SPC_K2_FOLD_MIN blocks use
+// the folding instantiation (C4 share: 64; C3: 23 at 5.5e-4 unfolded; C2: 18).
+constexpr int kFold = SPC_K2_FOLD;
+constexpr int kFoldPG = SPC_K2_FOLD_PG;  // the MHA (PG) rows' fold period
+constexpr int kFoldMinBlocks = SPC_K2_FOLD_MIN;
 #ifndef SPC_K2_CMMA
 #define SPC_K2_CMMA 0
 #endif
@@ -277,6 +302,7 @@ struct __align__(16) WarpSmem {
   }
   float4 sz[64];                                          // value (s*2^-q, z) pairs, vparams order (szidx)
   uint64_t bar[kS];
+  float zfold;  // the accumulator fold's z scale (kFold), read once per fold
   // float4 slot f of sz, low two bits XORed with the 8-slot row index (mod 4): the
   // decode stores (lane l -> 2l + h) and the PG loads (16 grp + 4 tq + 2 ks + h;
   // grp = gq >> 1 for 2 rows, gq & 3 for 1 row) hit 8 distinct 16-byte bank
@@ -800,7 +826,7 @@ __device__ void exact_segment_rows(const AttnArgs& a, const int split, const int
 template <int NR>
 constexpr int k2_maxreg() { return (SPC_K2_GQA_MAXREG > 0 && NR >= 4) ? SPC_K2_GQA_MAXREG : 128; }
 
-template <int BITS, int NR>
+template <int BITS, int NR, int FOLD>
 __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   constexpr int kSt = stages_of<BITS, NR>();
   // PACK: score MMA columns n = 2*row + plane (hi/lo of each row side by side),
@@ -938,6 +964,9 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   const float rz = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 4 + 3]);
   const int Ez = (VCO && rz > 0.f) ? ceil_log2(rz) - 14 : 0;
   const float zsc = pow2i(-Ez), z_out = pow2i(Ez);
+  // z sums at the value accumulator's scale (exact: powers of two); kept in
+  // shared memory, the main loop has no register to spare for it
+  if (lane == 0) ws.zfold = VCO ? pow2i(Ez - 24 - Ev) : pow2i(-24 - Ev);
   constexpr bool CMM = kCMma && HKB;
   // C-MMA: key zero-points as f16 hi + lo of z * 2^-Ezk (max <= 2^14); D * 2^(Ezk + aq) = C_j
   const float rzk = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 4 + 2]);
@@ -1001,6 +1030,45 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
     if ((it & 31) == 0 && it) {
       bm_cur = bm_next;
       bm_next = bm_window(blk + 32 * kWarps);
+    }
+    if (FOLD > 0 && it && (it % FOLD) == 0) {
+      // fold sum_t P z into the value accumulator (the epilogue's combination, early)
+      const float zfold = *reinterpret_cast<volatile float*>(&ws.zfold);
+      if constexpr (PG) {
+        float zt = zacc[0];  // lane partials -> the row group's sum (as after the loop)
+        zt += __shfl_xor_sync(0xffffffffu, zt, 1);
+        zt += __shfl_xor_sync(0xffffffffu, zt, 2);
+        const float zc0 = __shfl_sync(0xffffffffu, zt, 4 * (2 * tq)) * zfold;
+        const float zc1 = __shfl_sync(0xffffffffu, zt, 4 * ((2 * tq + 1) & 7)) * zfold;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = 2 * tq + e;
+            if (n < 4 * NR && n / NR == (mt >> 1)) {
+              dv[mt][e] += e ? zc1 : zc0;
+              dv[mt][2 + e] += e ? zc1 : zc0;
+            }
+          }
+        zacc[0] = 0.f;
+      } else if constexpr (VCO) {
+        const float zs0 = (zacc[0] + zacc[2 % (PG ? 1 : 4)]) * zfold;
+        const float zs1 = (zacc[1 % (PG ? 1 : 4)] + zacc[3 % (PG ? 1 : 4)]) * zfold;
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          const float z0 = __shfl_sync(0xffffffffu, zs0, 4 * gi + tq);
+          const float z1 = __shfl_sync(0xffffffffu, zs1, 4 * gi + tq);
+#pragma unroll
+          for (int mt = 2 * gi; mt < 2 * gi + 2; ++mt) {
+            dv[mt][0] += z0;
+            dv[mt][2] += z0;
+            dv[mt][1] += z1;
+            dv[mt][3] += z1;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < (PG ? 1 : 4); ++i) zacc[i] = 0.f;
+      }
     }
     const uint32_t bm = __shfl_sync(0xffffffffu, bm_cur, it & 31);
     mbar_wait(&ws.bar[st], phase);
@@ -1662,16 +1730,25 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   }
 }
 
-template <int BITS, int NR>
-void launch_fast_t(const AttnArgs& a, cudaStream_t st) {
+template <int BITS, int NR, int FOLD>
+void launch_fast_f(const AttnArgs& a, cudaStream_t st) {
   constexpr size_t smem = fast_smem_bytes<BITS, NR>();
   // two CTAs per SM (228 KB, 1 KB reserved per CTA) is the design point
   static_assert(smem * kMinBlocks <= 227 * 1024, "K2 shared memory exceeds kMinBlocks CTAs/SM");
-  static std::atomic<unsigned long long> done{0};  // one per <BITS, NR> instantiation
-  ensure_smem_attr(done, k_attend_fast<BITS, NR>, (int)smem);
+  static std::atomic<unsigned long long> done{0};  // one per <BITS, NR, FOLD> instantiation
+  ensure_smem_attr(done, k_attend_fast<BITS, NR, FOLD>, (int)smem);
   dim3 grid = kExactOrder == 0 ? dim3(a.nsplit + 1, a.G.H, a.G.batch)
                                 : dim3((a.nsplit + 1) * a.G.H * a.G.batch);
-  k_attend_fast<BITS, NR><<<grid, kThreads, smem, st>>>(a);
+  k_attend_fast<BITS, NR, FOLD><<<grid, kThreads, smem, st>>>(a);
+}
+
+// The fold's code costs K2 0.7-1.5% even where it never runs (C2), so it is a
+// separate instantiation, used when a warp walks more than kFoldMinBlocks blocks
+template <int BITS, int NR>
+void launch_fast_t(const AttnArgs& a, cudaStream_t st) {
+  constexpr int F = NR * 4 <= 8 ? kFoldPG : kFold;
+  if (F > 0 && a.blocks_per_split > kFoldMinBlocks * kWarps) launch_fast_f<BITS, NR, F>(a, st);
+  else launch_fast_f<BITS, NR, 0>(a, st);
 }
 
 

@@ -9,7 +9,7 @@
 // Also the contiguous pinned H2D peak (one cudaMemcpyAsync of the same bytes).
 //
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/h2d_probe.cu -o tools/h2d_probe
-//   tools/h2d_probe [row_bytes rows]   (default: the C2 and C3 per-layer gathers)
+//   tools/h2d_probe [row_bytes rows [slab_rows]]   (default: the C2 and C3 per-layer gathers)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -53,9 +53,9 @@ static void run(size_t row_bytes, int rows, size_t slab_rows) {
   CK(cudaHostGetDevicePointer((void**)&hd, h, 0));
   char* d = nullptr;
   CK(cudaMalloc((void**)&d, bytes));
-  std::vector<int> pos(rows);
+  std::vector<int> pos(rows);  // row index < 2^31
   std::mt19937 rng(7);
-  std::uniform_int_distribution<int> U(0, (int)slab_rows - 1);
+  std::uniform_int_distribution<long long> U(0, (long long)slab_rows - 1);
   for (int& p : pos) p = U(rng);
   int* dpos = nullptr;
   CK(cudaMalloc((void**)&dpos, rows * sizeof(int)));
@@ -107,8 +107,8 @@ static void run(size_t row_bytes, int rows, size_t slab_rows) {
 }
 
 int main(int argc, char** argv) {
-  if (argc == 3) {
-    run((size_t)std::atoll(argv[1]), std::atoi(argv[2]), 65536);
+  if (argc >= 3) {  // row_bytes rows [slab_rows]
+    run((size_t)std::atoll(argv[1]), std::atoi(argv[2]), argc > 3 ? (size_t)std::atoll(argv[3]) : 65536);
     return 0;
   }
   // C2 per layer-step: 16 seqs x ~47 new pins (73% of k=64) x (K, V) rows of H*d*2 = 8 KiB
