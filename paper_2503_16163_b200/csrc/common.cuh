@@ -123,8 +123,9 @@ struct GroupParams {
 __device__ inline GroupParams params_from_minmax(double lo, double hi, int bits) {
   GroupParams p;
   if (bits == 1) {
-    p.zero = __ddiv_rn(__dadd_rn(__dmul_rn(3.0, lo), hi), 4.0);
-    p.scale = __ddiv_rn(__dsub_rn(hi, lo), 2.0);
+    // x / 2^k == x * 2^-k bit for bit (one rounding of the same real value)
+    p.zero = __dmul_rn(__dadd_rn(__dmul_rn(3.0, lo), hi), 0.25);
+    p.scale = __dmul_rn(__dsub_rn(hi, lo), 0.5);
   } else {
     p.zero = lo;
     p.scale = __ddiv_rn(__dsub_rn(hi, lo), (double)((1 << bits) - 1));
@@ -139,7 +140,7 @@ __device__ inline uint32_t quantize_code(float xf, GroupParams p, int bits) {
   if (p.scale == 0.0) return 0u;  // degenerate group (quant.py:79-80)
   double x = (double)xf;
   if (bits == 1) {  // threshold at zero + scale/2, boundary maps up (quant.py:81-84)
-    return x >= __dadd_rn(p.zero, __ddiv_rn(p.scale, 2.0)) ? 1u : 0u;
+    return x >= __dadd_rn(p.zero, __dmul_rn(p.scale, 0.5)) ? 1u : 0u;
   }
   double c = rint(__ddiv_rn(__dsub_rn(x, p.zero), p.scale));  // half-even (quant.py:86)
   double top = (double)((1 << bits) - 1);

@@ -226,10 +226,12 @@ __global__ void __launch_bounds__(256) k_quantize_fast(Geo G, LayerBufs B, Quant
     float thr = CUDART_INF_F, rs = 0.f, zf = 0.f;
     if (p.scale != 0.0) {
       if (BITS == 1) {
-        thr = __double2float_ru(__dadd_rn(p.zero, __ddiv_rn(p.scale, 2.0)));
+        thr = __double2float_ru(__dadd_rn(p.zero, __dmul_rn(p.scale, 0.5)));
       } else {
         zf = (float)p.zero;  // = lo, exact
-        rs = (float)(1.0 / p.scale);
+        // fast code only: |error| << the 1e-5 boundary margin; an fp32-subnormal
+        // scale gives NaN, i.e. the float64 path for every code of the group
+        rs = (float)p.scale >= 1.17549435e-38f ? __frcp_rn((float)p.scale) : __int_as_float(0x7fc00000);
       }
     }
     if (key) {
@@ -412,10 +414,12 @@ __global__ void __launch_bounds__(256) k_quantize_fast2(Geo G, LayerBufs B, Quan
     float thr = CUDART_INF_F, rs = 0.f, zf = 0.f;
     if (p.scale != 0.0) {
       if (BITS == 1) {
-        thr = __double2float_ru(__dadd_rn(p.zero, __ddiv_rn(p.scale, 2.0)));
+        thr = __double2float_ru(__dadd_rn(p.zero, __dmul_rn(p.scale, 0.5)));
       } else {
         zf = (float)p.zero;  // = lo, exact
-        rs = (float)(1.0 / p.scale);
+        // fast code only: |error| << the 1e-5 boundary margin; an fp32-subnormal
+        // scale gives NaN, i.e. the float64 path for every code of the group
+        rs = (float)p.scale >= 1.17549435e-38f ? __frcp_rn((float)p.scale) : __int_as_float(0x7fc00000);
       }
     }
     if (key) {
