@@ -130,6 +130,24 @@ SPC_API int spc_predecode_layer(spc_cache* cache, int layer, const void* q, cons
  * fp32 (device), issues ticket (step, layer) and appends row 0. */
 SPC_API int spc_decode_layer(spc_cache* cache, int layer, int step, const void* q, const void* k_new,
                      const void* v_new, void* out, float* pinned_mass, void* stream);
+/* Step graphs (no reference counterpart: the launch side of engine.py:286-339's
+ * per-step layer loop).  spc_graph_begin starts capturing `stream`; the
+ * spc_decode_layer calls that follow (same stream; no other entry point until
+ * spc_graph_launch, SPC_EPROTO otherwise) are recorded with their copy- and
+ * selection-stream work instead of launched; spc_graph_launch joins those
+ * streams, refreshes the cache's executable graph with the new kernel
+ * arguments (cudaGraphExecUpdate; a step of another shape -- a migration, a
+ * different split plan -- is instantiated afresh) and launches it on `stream`.
+ * Results equal the eager calls'.  Not with spc_profile on or with
+ * spc_set_agg_reduce(c, 1). */
+SPC_API int spc_graph_begin(spc_cache* cache, void* stream);
+SPC_API int spc_graph_launch(spc_cache* cache, void* stream);
+/* Ends an open capture without launching.  The decode calls already captured
+ * have advanced the cache's lengths and tickets, so it returns SPC_EPROTO and
+ * the cache must be destroyed. */
+SPC_API int spc_graph_abort(spc_cache* cache);
+/* Instantiations and in-place updates of the step graph so far. */
+SPC_API int spc_graph_stats(const spc_cache* cache, int64_t* instantiations, int64_t* updates);
 /* The last ticket of `layer` (PrefetchTicket, transfer.py:50-55): picked
  * positions device int32 [batch][units][k] (-1 padded, ascending) and new-pin
  * counts device int32 [batch][units].  Ordered after the selection on `stream`. */

@@ -47,6 +47,10 @@ _SIGS = {
     "spc_pin": (_I, [_P, _I, _I, _I, _P, _I, _P, _P, _P]),
     "spc_predecode_layer": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "spc_decode_layer": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "spc_graph_begin": (_I, [_P, _P]),
+    "spc_graph_launch": (_I, [_P, _P]),
+    "spc_graph_abort": (_I, [_P]),
+    "spc_graph_stats": (_I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "spc_ticket": (_I, [_P, _I, _P, _P, _P]),
     "spc_debug_agg": (_I, [_P, _I, _P, _P]),
     "spc_debug_output_f32": (_I, [_P, _I]),

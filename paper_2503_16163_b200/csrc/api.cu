@@ -120,6 +120,14 @@ struct spc_cache {
     cudaEvent_t p0 = nullptr;
   };
   std::vector<Pending> pend;
+  // step graphs (spc_graph_begin / spc_graph_launch): the decode calls between
+  // them are captured from the caller's stream, then replayed as one graph
+  bool capturing = false, capture_failed = false;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  int gexec_last = 0;
+  cudaEvent_t ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t graph_updates = 0, graph_instantiations = 0;
 };
 
 namespace {
@@ -143,7 +151,15 @@ int check_layer(const spc_cache* c, int layer) {
   return SPC_OK;
 }
 
-int check_not_pending(const spc_cache* c, int layer) {
+int no_capture(const spc_cache* c) {
+  if (c->capturing)
+    return fail(SPC_EPROTO, "only spc_decode_layer may be called between spc_graph_begin and spc_graph_launch");
+  return SPC_OK;
+}
+
+int check_not_pending(const spc_cache* c, int layer, bool capture_ok = false) {
+  if (!capture_ok)
+    if (int rc = no_capture(c)) return rc;
   if (c->pend[layer].on)
     return fail(SPC_EPROTO, "layer " + std::to_string(layer) +
                                 ": the aggregate awaits its cross-rank reduction (call spc_finish_layer)");
@@ -514,9 +530,16 @@ int spc_cache_create(const spc_dims* d, int device, spc_cache** out) {
 int spc_cache_destroy(spc_cache* c) {
   if (!c) return SPC_OK;
   cudaSetDevice(c->device);
+  if (c->capturing) {  // abandon an open capture
+    cudaGraph_t g = nullptr;
+    if (cudaStreamEndCapture(c->cap_stream, &g) == cudaSuccess && g) cudaGraphDestroy(g);
+    cudaGetLastError();
+  }
   cudaDeviceSynchronize();
   for (void* p : c->dev_allocs) cudaFree(p);
   if (c->dbg_out) cudaFree(c->dbg_out);
+  for (auto g : c->gexec) if (g) cudaGraphExecDestroy(g);
+  for (auto e : c->ev_join) if (e) cudaEventDestroy(e);
   if (c->host_k) cudaFreeHost(c->host_k);
   if (c->host_v) cudaFreeHost(c->host_v);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -563,6 +586,7 @@ int spc_set_prefetch_inflight(spc_cache* c, int64_t bytes) {
 
 int spc_prefill(spc_cache* c, int layer, const void* K, const void* V, int n, void* stream) {
   if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = no_capture(c)) return rc;
   const Geo& G = c->G;
   cudaStream_t st = (cudaStream_t)stream;
   if (c->n[layer] != 0) return fail(SPC_EPROTO, "prefill requires an empty layer");
@@ -590,6 +614,7 @@ int spc_prefill(spc_cache* c, int layer, const void* K, const void* V, int n, vo
 int spc_append(spc_cache* c, int layer, const void* k_rows, const void* v_rows, int64_t seq_stride,
                void* stream) {
   if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = no_capture(c)) return rc;
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_pf[layer], 0));
   return append_rows(c, layer, k_rows, v_rows, seq_stride, (cudaStream_t)stream);
@@ -597,6 +622,7 @@ int spc_append(spc_cache* c, int layer, const void* k_rows, const void* v_rows, 
 
 int spc_migrate(spc_cache* c, int layer, void* stream) {
   if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = no_capture(c)) return rc;
   if (c->n[layer] - c->f[layer] < c->G.g)  // kvcache.py:175-177
     return fail(SPC_EINVAL, "not enough residual tokens to migrate");
   CUDA_TRY(cudaSetDevice(c->device));
@@ -666,9 +692,24 @@ int spc_decode_layer(spc_cache* c, int layer, int step, const void* q, const voi
   if (c->ticket[layer] != step - 1)  // transfer.py:96-100
     return fail(SPC_EPROTO, "no ticket was issued at step " + std::to_string(step - 1) + " for layer " +
                                 std::to_string(layer));
-  if (int rc = check_not_pending(c, layer)) return rc;
+  if (int rc = check_not_pending(c, layer, true)) return rc;
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (c->capturing) {
+    // in a step graph the previous step's ticket is complete before the graph
+    // starts (graph launches are stream-ordered; spc_graph_begin orders the
+    // first one after any eager ticket), so there is no await_layer edge
+    if (st != c->cap_stream)
+      return fail(SPC_EINVAL, "spc_decode_layer during capture must use the stream given to spc_graph_begin");
+    c->ticket[layer] = -1;
+    int rc = run_layer(c, layer, 2, q, k_new, v_new, out, pinned_mass, st, true);
+    if (rc) {
+      c->capture_failed = true;
+      return rc;
+    }
+    c->ticket[layer] = step;
+    return SPC_OK;
+  }
   cudaEvent_t w0 = nullptr, w1 = nullptr;
   if (c->prof) {  // exposed prefetch: compute-stream time spent waiting on the ticket
     w0 = prof_event(c);
@@ -688,8 +729,115 @@ int spc_decode_layer(spc_cache* c, int layer, int step, const void* q, const voi
   return SPC_OK;
 }
 
+int spc_graph_begin(spc_cache* c, void* stream) {
+  if (!c) return fail(SPC_EINVAL, "null cache");
+  if (c->capturing) return fail(SPC_EPROTO, "spc_graph_begin: already capturing");
+  if (c->prof) return fail(SPC_EPROTO, "spc_graph_begin: live profiling (spc_profile) is on");
+  if (c->agg_ext) return fail(SPC_EPROTO, "spc_graph_begin: the cross-rank aggregate reduction is on");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!st) return fail(SPC_EINVAL, "spc_graph_begin: the legacy default stream cannot be captured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  // eager tickets still in flight on the copy streams come before the graph
+  for (int l = 0; l < c->G.layers; ++l) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_pf[l], 0));
+  CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  c->capturing = true;
+  c->capture_failed = false;
+  c->cap_stream = st;
+  return SPC_OK;
+}
+
+// Joins the side streams back into the capture, ends it, refreshes the
+// executable graph (cudaGraphExecUpdate: same topology, new kernel arguments;
+// a step with a different topology -- a migration, another split plan's
+// kernel -- instantiates afresh) and launches it on the capture stream.
+int spc_graph_launch(spc_cache* c, void* stream) {
+  if (!c) return fail(SPC_EINVAL, "null cache");
+  if (!c->capturing) return fail(SPC_EPROTO, "spc_graph_launch without spc_graph_begin");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (st != c->cap_stream) return fail(SPC_EINVAL, "spc_graph_launch: not the stream given to spc_graph_begin");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const cudaStream_t side[4] = {c->copy_stream, c->copy_stream2, c->sel_stream, c->sel_stream2};
+  cudaError_t err = cudaSuccess;
+  for (int i = 0; i < 4 && err == cudaSuccess; ++i) {
+    if (!side[i]) continue;
+    cudaStreamCaptureStatus cs_status = cudaStreamCaptureStatusNone;
+    err = cudaStreamIsCapturing(side[i], &cs_status);
+    if (err == cudaSuccess && cs_status == cudaStreamCaptureStatusActive) {
+      if (!c->ev_join[i]) err = cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming);
+      if (err == cudaSuccess) err = cudaEventRecord(c->ev_join[i], side[i]);
+      if (err == cudaSuccess) err = cudaStreamWaitEvent(st, c->ev_join[i], 0);
+    }
+  }
+  cudaGraph_t graph = nullptr;
+  cudaError_t e_end = cudaStreamEndCapture(st, &graph);
+  c->capturing = false;
+  if (err == cudaSuccess) err = e_end;
+  if (err != cudaSuccess || c->capture_failed) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    if (c->capture_failed) return fail(SPC_EPROTO, "a decode call failed during capture; nothing was launched");
+    return fail(SPC_ECUDA, std::string("step graph capture: ") + cudaGetErrorString(err));
+  }
+  // two executable graphs: the steady step and the other shape that recurs (a
+  // step with a migration), so alternating shapes update in place too
+  int slot = -1;
+  for (int k = 0; k < 2 && slot < 0; ++k) {
+    const int i = (c->gexec_last + k) & 1;
+    if (!c->gexec[i]) continue;
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(c->gexec[i], graph, &info) == cudaSuccess) {
+      slot = i;
+      c->graph_updates += 1;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  if (slot < 0) {
+    slot = c->gexec[c->gexec_last] ? (c->gexec_last ^ 1) : c->gexec_last;  // the slot not used last
+    if (c->gexec[slot]) cudaGraphExecDestroy(c->gexec[slot]);
+    c->gexec[slot] = nullptr;
+    cudaError_t e = cudaGraphInstantiate(&c->gexec[slot], graph, 0);
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      c->gexec[slot] = nullptr;
+      return fail(SPC_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    }
+    c->graph_instantiations += 1;
+  }
+  c->gexec_last = slot;
+  cudaGraphDestroy(graph);
+  CUDA_TRY(cudaGraphLaunch(c->gexec[slot], st));
+  // later eager work that awaits a layer's ticket (the next eager decode,
+  // export, materialize, ...) waits on ev_pf: point it past the graph
+  for (int l = 0; l < c->G.layers; ++l) CUDA_TRY(cudaEventRecord(c->ev_pf[l], st));
+  return SPC_OK;
+}
+
+int spc_graph_abort(spc_cache* c) {
+  if (!c) return fail(SPC_EINVAL, "null cache");
+  if (!c->capturing) return SPC_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
+  if (g) cudaGraphDestroy(g);
+  c->capturing = false;
+  cudaGetLastError();
+  // the captured decode calls advanced the host-side state (lengths, tickets)
+  // without running: the cache is no longer consistent with the device
+  return fail(SPC_EPROTO, std::string("step graph aborted (") + cudaGetErrorString(e) +
+                              "): the cache's host state ran ahead of the device; destroy it");
+}
+
+int spc_graph_stats(const spc_cache* c, int64_t* instantiations, int64_t* updates) {
+  if (!c) return fail(SPC_EINVAL, "null cache");
+  if (instantiations) *instantiations = c->graph_instantiations;
+  if (updates) *updates = c->graph_updates;
+  return SPC_OK;
+}
+
 int spc_set_agg_reduce(spc_cache* c, int enable) {
   if (!c) return fail(SPC_EINVAL, "null cache");
+  if (int rc = no_capture(c)) return rc;
   for (int l = 0; l < c->G.layers; ++l)
     if (c->pend[l].on) return fail(SPC_EPROTO, "a layer is waiting for spc_finish_layer");
   c->agg_ext = enable != 0;
@@ -707,6 +855,7 @@ int spc_agg_buffer(spc_cache* c, int layer, float** agg, int64_t* count, void** 
 
 int spc_finish_layer(spc_cache* c, int layer) {
   if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = no_capture(c)) return rc;
   spc_cache::Pending& p = c->pend[layer];
   if (!p.on)
     return fail(SPC_EPROTO, "spc_finish_layer without a pending aggregate for layer " + std::to_string(layer));
@@ -742,6 +891,7 @@ int spc_debug_agg(spc_cache* c, int layer, float* agg, void* stream) {
 
 int spc_debug_output_f32(spc_cache* c, int enable) {
   if (!c) return fail(SPC_EINVAL, "null cache");
+  if (int rc = no_capture(c)) return rc;
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaDeviceSynchronize());
   if (enable && !c->dbg_out) {
@@ -796,6 +946,7 @@ int spc_export_packed(spc_cache* c, int layer, int seq, uint8_t* kc, uint16_t* k
 int spc_slow_fetch(spc_cache* c, int layer, int seq, const int32_t* positions, int npos, void* k_out,
                    void* v_out) {
   if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = no_capture(c)) return rc;
   const Geo& G = c->G;
   if (seq < 0 || seq >= G.batch) return fail(SPC_EINVAL, "seq out of range");
   for (int i = 0; i < npos; ++i)  // kvcache.py:250-252
@@ -816,6 +967,7 @@ int spc_slow_fetch(spc_cache* c, int layer, int seq, const int32_t* positions, i
 int spc_profile(spc_cache* c, int enable, double* attn_ms, int64_t* attn_launches, double* sel_ms,
                 int64_t* sel_launches, int64_t* launches) {
   if (!c) return fail(SPC_EINVAL, "null cache");
+  if (int rc = no_capture(c)) return rc;
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaDeviceSynchronize());
   double a = 0, s = 0;

@@ -15,6 +15,8 @@ the same layer waits on that ticket's event (await_layer).
 """
 from __future__ import annotations
 
+import contextlib
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -118,6 +120,31 @@ class SpeculativeLayerDecoder:
         self._keep = (q, k, v)
         self._finish(layer)
         return LayerResult(out, pinned_mass)
+
+    @contextlib.contextmanager
+    def step_graph(self):
+        """Capture the decode_layer calls inside the block and launch them as one
+        CUDA graph at its end (spc_graph_begin / spc_graph_launch): one graph
+        launch per step instead of the per-layer kernels and cross-stream
+        events.  The current stream must not be the legacy default stream;
+        inputs must be device bf16 tensors and out / pinned_mass preallocated
+        (nothing may allocate or copy from the host while capturing)."""
+        lib, h = _lib.lib(), self.cache.handle
+        s = current_stream(self._dev)
+        _lib.check(lib.spc_graph_begin(h, s))
+        try:
+            yield self
+        except BaseException:
+            lib.spc_graph_abort(h)
+            raise
+        _lib.check(lib.spc_graph_launch(h, s))
+
+    def graph_stats(self):
+        """(instantiations, in-place updates) of the step graph."""
+        import ctypes
+        i, u = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib().spc_graph_stats(self.cache.handle, ctypes.byref(i), ctypes.byref(u)))
+        return i.value, u.value
 
     def ticket(self, layer: int):
         """(picked int32 [batch, units, k] ascending -1 padded, new_count int32 [batch, units])
