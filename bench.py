@@ -520,6 +520,8 @@ def run_gpu_arm(args, cfg):
 
     rank, world, local, local_world = dist_env()
     device, group, part, lcfg, reduce_agg = setup_ranks(args, cfg)
+    if args.graph and reduce_agg:
+        raise SystemExit("--graph does not combine with the cross-rank aggregate reduction (--shard heads)")
 
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -531,7 +533,10 @@ def run_gpu_arm(args, cfg):
         torch.cuda.set_stream(torch.cuda.Stream(device, priority=args.compute_priority))
 
     W, K = args.warmup, args.steps
-    total_steps = 2 * (W + K)  # device-timed pass + end-to-end pass
+    if args.graph and not args.compute_priority:
+        torch.cuda.set_stream(torch.cuda.Stream(device))  # the legacy default stream cannot be captured
+    # device-timed pass + end-to-end pass (+ the eager profiled pass of --graph)
+    total_steps = (3 if args.graph else 2) * (W + K)
     host_layers = args.host_layers or plan_host_layers(cfg, local_world)
     budget = CacheBudget(bits=cfg["bits"], group_size=cfg["group"], residual=cfg["residual"],
                          prefetch_k=cfg["topk"], context_length=cfg["ctx"] + total_steps + 64)
@@ -559,13 +564,17 @@ def run_gpu_arm(args, cfg):
     lib, h = _lib.lib(), cache.handle
     stream = torch.cuda.current_stream(device).cuda_stream
 
-    def step_device(t, qt, kt, vt):
+    def step_device(t, qt, kt, vt, graph=False):
+        if graph:
+            _lib.check(lib.spc_graph_begin(h, stream))
         for layer in range(L):
             _lib.check(lib.spc_decode_layer(h, layer, t, qt[layer].data_ptr(), kt[layer].data_ptr(),
                                             vt[layer].data_ptr(), out[layer].data_ptr(),
                                             pm[layer].data_ptr(), stream))
             if reduce_layer:
                 reduce_layer(layer)
+        if graph:
+            _lib.check(lib.spc_graph_launch(h, stream))
 
     # predecode (Alg. 2): first tickets
     for layer in range(L):
@@ -597,15 +606,32 @@ def run_gpu_arm(args, cfg):
     torch.cuda.synchronize(device)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     newpins = []
+    if args.graph:
+        # K2 / prefetch event timings need the eager path (profiling events
+        # cannot sit inside a step graph): one profiled eager pass first
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        for _ in range(K):
+            step_device(t, q[t], k_new[t], v_new[t])
+            t += 1
+        eb.record()
+        torch.cuda.synchronize(device)
+        prof_eager = profile(0)
+        eager_ms = ea.elapsed_time(eb)
+        for _ in range(W):
+            step_device(t, q[t], k_new[t], v_new[t], graph=True)
+            t += 1
+        torch.cuda.synchronize(device)
     with ClockSampler(torch.device(device).index) as clocks:
         ev0.record()
         for _ in range(K):
-            step_device(t, q[t], k_new[t], v_new[t])
+            step_device(t, q[t], k_new[t], v_new[t], graph=args.graph)
             t += 1
         ev1.record()
         torch.cuda.synchronize(device)
     elapsed_ms = ev0.elapsed_time(ev1)
-    attn_ms, attn_n, sel_ms, sel_n, launches = profile(0)
+    attn_ms, attn_n, sel_ms, sel_n, launches = prof_eager if args.graph else profile(0)
+    prof_ms = eager_ms if args.graph else elapsed_ms  # the pass the event timings come from
     wait_ms = lib.spc_profile_wait_ms(h)
     pf_ms = lib.spc_profile_prefetch_ms(h)
     pf_wall_ms = lib.spc_profile_prefetch_wall_ms(h)
@@ -676,15 +702,48 @@ def run_gpu_arm(args, cfg):
         done_out[sb] = torch.cuda.Event()
         done_out[sb].record(cs_out)
 
+    if args.graph:
+        # one packed transfer each way per step: q|k|v in, out|pinned_mass out
+        def packed(shapes_dtypes, dev):
+            sizes = [int(np.prod(sh)) * torch.empty((), dtype=dt).element_size() for sh, dt in shapes_dtypes]
+            buf = torch.empty(sum(sizes), dtype=torch.uint8, device=dev)
+            views, o = [], 0
+            for (sh, dt), n in zip(shapes_dtypes, sizes):
+                views.append(buf[o:o + n].view(dt).view(sh))
+                o += n
+            return buf, views
+        in_spec = [(tuple(q[0].shape), torch.bfloat16), (tuple(k_new[0].shape), torch.bfloat16),
+                   (tuple(v_new[0].shape), torch.bfloat16)]
+        in_dev, (qg, kg, vg) = packed(in_spec, device)
+        out_dev, (og, pmg) = packed([(tuple(out.shape), torch.bfloat16), (tuple(pm.shape), torch.float32)], device)
+        out_host = torch.empty(out_dev.numel(), dtype=torch.uint8).pin_memory()
+        g_in = []
+        for i in range(len(e2e_in)):
+            hb, (hq, hk, hv) = packed(in_spec, "cpu")
+            hq.copy_(e2e_in[i][0]), hk.copy_(e2e_in[i][1]), hv.copy_(e2e_in[i][2])
+            g_in.append(hb.pin_memory())
+
+    def step_e2e_graph(i, tt):
+        # one graph per step: H2D of the step's inputs, the layers, D2H of the results
+        _lib.check(lib.spc_graph_begin(h, stream))
+        _lib.check(lib.spc_copy_async(in_dev.data_ptr(), g_in[i].data_ptr(), in_dev.numel(), stream))
+        for layer in range(L):
+            _lib.check(lib.spc_decode_layer(h, layer, tt, qg[layer].data_ptr(), kg[layer].data_ptr(),
+                                            vg[layer].data_ptr(), og[layer].data_ptr(), pmg[layer].data_ptr(),
+                                            stream))
+        _lib.check(lib.spc_copy_async(out_host.data_ptr(), out_dev.data_ptr(), out_dev.numel(), stream))
+        _lib.check(lib.spc_graph_launch(h, stream))
+
+    run_e2e = step_e2e_graph if args.graph else step_e2e
     for i in range(W):
-        step_e2e(i, t)
+        run_e2e(i, t)
         t += 1
     torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
     w0 = time.perf_counter()
     for i in range(W, W + K):
-        step_e2e(i, t)
+        run_e2e(i, t)
         t += 1
     torch.cuda.synchronize(device)
     e2e_s = time.perf_counter() - w0
@@ -732,10 +791,10 @@ def run_gpu_arm(args, cfg):
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": "K2 attend (per layer launch, all sequences)",
                      "algorithmic_bytes_per_launch": ab["hbm"], "avg_launch_ms": attn_avg_ms,
-                     "launches": attn_n, "kernel_share_of_step": attn_ms / max(1e-9, elapsed_ms)},
+                     "launches": attn_n, "kernel_share_of_step": attn_ms / max(1e-9, prof_ms)},
         "prefetch": {"new_pin_fraction": h2d_pf / max(1, cfg["topk"] * cfg["batch"] * cfg["layers"] * cache.row_bytes(1)),
                      "h2d_bytes_per_step": h2d_pf,
-                     "exposed_ms_per_step": wait_ms / K, "exposed_fraction": wait_ms / max(1e-9, elapsed_ms),
+                     "exposed_ms_per_step": wait_ms / K, "exposed_fraction": wait_ms / max(1e-9, prof_ms),
                      "copy_stream_ms_per_step": sel_ms / K, "prefetch_kernel_ms_per_step": pf_ms / K,
                      "prefetch_wall_ms_per_step": pf_wall_ms / K,
                      "h2d_gbs": (h2d_pf / 1e9) / max(1e-9, pf_wall_ms / K / 1e3),
@@ -747,11 +806,19 @@ def run_gpu_arm(args, cfg):
                                 "memory, DMA and zero-copy kernel, same process"},
         "e2e": {"value": tokens / e2e_s,
                 "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "how": "through spc_decode_layer (C ABI) with pinned host inputs/outputs; per group of 8 "
-                       "layers, H2D of its q/k/v and D2H of its outputs on two copy streams overlapping the "
-                       "other groups' decode, two buffer sets so consecutive steps' copies overlap too; "
-                       "wall clock around synchronize, max over ranks"},
+                "how": ("one step graph per step (spc_graph_begin / spc_graph_launch) holding the H2D of the "
+                        "step's q/k/v from pinned host memory (spc_copy_async), every layer's spc_decode_layer and "
+                        "the D2H of its outputs; wall clock around synchronize, max over ranks") if args.graph else
+                       ("through spc_decode_layer (C ABI) with pinned host inputs/outputs; per group of 8 "
+                        "layers, H2D of its q/k/v and D2H of its outputs on two copy streams overlapping the "
+                        "other groups' decode, two buffer sets so consecutive steps' copies overlap too; "
+                        "wall clock around synchronize, max over ranks")},
         "gpu_launches": launches,
+        **({"graph": {"step_graphs": True, "instantiations_updates": dec.graph_stats(),
+                      "eager_ms_per_step": eager_ms / K,
+                      "timings_from": "roofline, prefetch and gpu_launches from an eager profiled pass of the "
+                                      "same K steps (profiling events cannot sit inside a step graph)"}}
+           if args.graph else {}),
         "clocks": clocks.summary(),
         "topk_parity": {"band": TIE_BAND, **band, **parity_record(args.config)},
         "setup_s": setup_s,
@@ -982,6 +1049,9 @@ def main():
     ap.add_argument("--pf-inflight", type=int, default=0,
                     help="PCIe gather bytes in flight (spc_set_prefetch_inflight; 0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="issue each step as one CUDA graph (spc_graph_begin/launch), the e2e pass with its "
+                         "host copies inside; K2/prefetch timings then come from an eager profiled pass")
     ap.add_argument("--shard", default="auto", choices=["auto", "heads", "seq", "replicas"],
                     help="multi-GPU partition of the global batch: auto = by KV head, then by sequence "
                          "where heads run out (default, the north star's rule); heads; seq; or replicas "

@@ -146,6 +146,10 @@ SPC_API int spc_graph_launch(spc_cache* cache, void* stream);
  * have advanced the cache's lengths and tickets, so it returns SPC_EPROTO and
  * the cache must be destroyed. */
 SPC_API int spc_graph_abort(spc_cache* cache);
+/* A step's host I/O (the engine's inputs in, outputs out): cudaMemcpyAsync
+ * of `bytes`, direction from the pointers (pinned host or device), on
+ * `stream`; inside a step graph it is captured with the decode calls. */
+SPC_API int spc_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 /* Instantiations and in-place updates of the step graph so far. */
 SPC_API int spc_graph_stats(const spc_cache* cache, int64_t* instantiations, int64_t* updates);
 /* The last ticket of `layer` (PrefetchTicket, transfer.py:50-55): picked

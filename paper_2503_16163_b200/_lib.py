@@ -50,6 +50,7 @@ _SIGS = {
     "spc_graph_begin": (_I, [_P, _P]),
     "spc_graph_launch": (_I, [_P, _P]),
     "spc_graph_abort": (_I, [_P]),
+    "spc_copy_async": (_I, [_P, _P, _I64, _P]),
     "spc_graph_stats": (_I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "spc_ticket": (_I, [_P, _I, _P, _P, _P]),
     "spc_debug_agg": (_I, [_P, _I, _P, _P]),

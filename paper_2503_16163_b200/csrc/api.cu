@@ -828,6 +828,12 @@ int spc_graph_abort(spc_cache* c) {
                               "): the cache's host state ran ahead of the device; destroy it");
 }
 
+int spc_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes && (!dst || !src))) return fail(SPC_EINVAL, "spc_copy_async: bad arguments");
+  if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  return SPC_OK;
+}
+
 int spc_graph_stats(const spc_cache* c, int64_t* instantiations, int64_t* updates) {
   if (!c) return fail(SPC_EINVAL, "null cache");
   if (instantiations) *instantiations = c->graph_instantiations;

@@ -30,3 +30,20 @@ def test_bench_two_ranks_head_sharded():
     assert d["rank_share"]["kv_heads"] == 4 and d["rank_share"]["q_heads"] == 16 and d["rank_share"]["batch"] == 8
     assert "kv-heads x2" in d["config"]["parallelism"]
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+
+
+@pytest.mark.timeout(600)
+def test_bench_step_graphs():
+    """`--graph`: every step (and every e2e step with its host copies) as one
+    CUDA graph; the line carries the graph stats and the eager pass's timings."""
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c1", "--graph",
+                          "--steps", "20", "--warmup", "3", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=500, env=env, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    inst, upd = d["graph"]["instantiations_updates"]
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["roofline"]["frac"] > 0
+    assert 1 <= inst <= 8 and upd >= 30, (inst, upd)
