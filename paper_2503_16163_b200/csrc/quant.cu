@@ -351,7 +351,11 @@ __global__ void __launch_bounds__(256) k_quantize_fast2(Geo G, LayerBufs B, Quan
   __shared__ __align__(16) uint16_t tk[g * LD];
   __shared__ __align__(16) uint16_t tv[g * LD];
   __shared__ __align__(16) uint8_t ck[g * d];   // key codes [t][c]
-  __shared__ __align__(16) uint8_t cv[d * 34];  // value codes [c][t], 34-byte rows (17 words: odd)
+  // value codes [c][t], 42-byte rows: conflict-free for both the code stores
+  // (lanes: channels 2l, token t) and the packing loads (the fragment order's
+  // (mt, gq, tq) lanes); 34-byte rows left the packing loads 2-way
+  constexpr int CVS = 42;
+  __shared__ __align__(16) uint8_t cv[d * CVS];
   __shared__ float kz[d], krs[d], kthr[d];
   __shared__ double kz64[d], ks64[d];
   __shared__ float vz[g * 4], vrs[g * 4], vthr[g * 4];
@@ -394,7 +398,8 @@ __global__ void __launch_bounds__(256) k_quantize_fast2(Geo G, LayerBufs B, Quan
       atomicMax(reinterpret_cast<unsigned*>(&s_rk), __float_as_uint(hi - lo));
       atomicMax(reinterpret_cast<unsigned*>(&s_ak), __float_as_uint(fmaxf(fabsf(lo), fabsf(hi))));
       gidx = c;
-    } else {  // 32 channels of token t, rotated start
+    } else {  // 32 channels of token t, rotated start (a 2j rotation is conflict-free
+      // but costs 2% more instructions than the 2-way conflicts it removes)
       const int i = tid - 128, t = i >> 2, j = i & 3;
       const uint16_t* r = tv + t * LD + 32 * j;
       lo = hi = bf(r[j]);
@@ -472,8 +477,8 @@ __global__ void __launch_bounds__(256) k_quantize_fast2(Geo G, LayerBufs B, Quan
         if (n3) v1 = quantize_code(xv1, GroupParams{vz64[gi], vs64[gi]}, 2);
       }
       *reinterpret_cast<uint16_t*>(ck + t * d + c) = (uint16_t)(k0 | (k1 << 8));
-      cv[c * 34 + t] = (uint8_t)v0;
-      cv[(c + 1) * 34 + t] = (uint8_t)v1;
+      cv[c * CVS + t] = (uint8_t)v0;
+      cv[(c + 1) * CVS + t] = (uint8_t)v1;
     }
   }
   __syncthreads();
@@ -528,7 +533,7 @@ __global__ void __launch_bounds__(256) k_quantize_fast2(Geo G, LayerBufs B, Quan
         const int q = r & 3;
         const int c = 16 * mt + 8 * rh + gq;
         const int t = 16 * (q >> 1) + 8 * (q & 1) + 2 * tq;
-        const uint32_t x = *reinterpret_cast<const uint16_t*>(cv + c * 34 + t);
+        const uint32_t x = *reinterpret_cast<const uint16_t*>(cv + c * CVS + t);
         const uint32_t m = BITS == 2 ? 3u : 1u;
         word |= ((x & m) << (BITS * r)) | (((x >> 8) & m) << (16 + BITS * r));
       }
