@@ -825,11 +825,41 @@ def run_gpu_arm(args, cfg):
         "cpu_baseline": cpu_base,
     }
     if rank == 0:
+        if getattr(args, "ctx128k", None) is not None:
+            line["ctx_128k"] = args.ctx128k
         print(json.dumps(line), flush=True)
     cache.close()
     if dist.is_initialized():
         dist.destroy_process_group()
     return 0
+
+
+def run_ctx128k_companion(args) -> dict:
+    """The metric's 128k half in the default (driver-run) line: the same bench
+    at C3 (BASELINE configs[2] on one GPU: GQA 8 KV heads, 128k, batch 8,
+    1-bit, k128) in a child process, run BEFORE the headline config so each
+    process owns the GPU and the pinned host memory alone.  Returns a compact
+    summary of the child's JSON line (or the reason it is missing)."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--config", "c3", "--steps", str(args.steps),
+           "--warmup", str(args.warmup), "--no-cpu-baseline", "--no-ctx128k"]
+    try:
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        lines = [x for x in res.stdout.splitlines() if x.startswith("{")]
+        if res.returncode != 0 or not lines:
+            return {"unavailable": "C3 child exited %d: %s" % (res.returncode, res.stderr.strip()[-300:])}
+        d = json.loads(lines[-1])
+    except (subprocess.TimeoutExpired, ValueError, OSError) as e:
+        return {"unavailable": "C3 child failed: %r" % (e,)}
+    rf, pf = d.get("roofline", {}), d.get("prefetch", {})
+    return {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
+            "ms_per_step": d["ms_per_step"], "steps": d["steps"], "warmup": d["warmup"],
+            "e2e": d.get("e2e", {}).get("value"),
+            "roofline": {k: rf.get(k) for k in ("achieved", "peak", "frac", "traffic", "avg_launch_ms",
+                                                  "kernel_share_of_step")},
+            "prefetch": {k: pf.get(k) for k in ("exposed_fraction", "h2d_gbs", "h2d_frac")},
+            "gpu_launches": d.get("gpu_launches"), "clocks": d.get("clocks"),
+            "topk_parity": d.get("topk_parity"),
+            "how": "bench.py --config c3 in a child process before the headline run, same steps/warmup"}
 
 
 def setup_ranks(args, cfg):
@@ -1049,6 +1079,8 @@ def main():
     ap.add_argument("--pf-inflight", type=int, default=0,
                     help="PCIe gather bytes in flight (spc_set_prefetch_inflight; 0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ctx128k", action="store_true",
+                    help="skip the C3 (128k) companion measurement of the default single-GPU run")
     ap.add_argument("--graph", action="store_true",
                     help="issue each step as one CUDA graph (spc_graph_begin/launch), the e2e pass with its "
                          "host copies inside; K2/prefetch timings then come from an eager profiled pass")
@@ -1074,6 +1106,10 @@ def main():
         return run_dry(args, cfg)
     if args.full_decoder:
         return run_full_decoder(args, cfg)
+    args.ctx128k = None
+    if (args.config == "c2" and not args.no_ctx128k and "WORLD_SIZE" not in os.environ and args.gpus == 1
+            and not args.share and not args.graph):
+        args.ctx128k = run_ctx128k_companion(args)
     return run_gpu_arm(args, cfg)
 
 
