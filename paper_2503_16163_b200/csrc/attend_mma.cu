@@ -816,6 +816,9 @@ __device__ void exact_segment_rows(const AttnArgs& a, const int split, const int
   }
 }
 
+#ifndef SPC_K2_UWARP_NR
+#define SPC_K2_UWARP_NR 4  // widest row count whose warp index is made uniform (see k_attend_fast)
+#endif
 #ifndef SPC_K2_GQA_MAXREG
 #define SPC_K2_GQA_MAXREG 0
 #endif
@@ -863,7 +866,13 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
     else exact_segment_fast<NR>(a, split, h, b, smem_raw);
     return;
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: the compiler then treats it (and the block
+  // index, ring stage and record address derived from it) as warp-uniform, so
+  // the per-block bulk copy takes its operands from uniform registers instead
+  // of a divergent R2UR waterfall loop around UBLKCP.  Not for the 8-row GQA
+  // instantiations: the uniform copies push them over 128 registers (spills).
+  const int warp = NR <= SPC_K2_UWARP_NR ? __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0) : (int)(threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
   WarpSmem<BITS, NR>& ws = reinterpret_cast<WarpSmem<BITS, NR>*>(smem_raw)[warp];
 
@@ -883,6 +892,27 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
     const unsigned bar = bar0 + 8u * st;
     mbar_expect_tx_u32(bar, SL::bytes);  // the whole block record, one bulk copy
     tma_load_u32(stage0 + kStageBytes * st, src, SL::bytes, bar);
+  };
+  // refill of a consumed stage (async proxy after the lanes' generic reads).  With a
+  // warp-uniform warp index the whole warp runs it and elect.sync picks the issuing
+  // lane inside the asm: no divergent branch, so no ELECT loop around UBLKCP.
+  auto refill = [&](const uint32_t* src, int st, bool more) {
+    if (NR <= SPC_K2_UWARP_NR) {
+      if (more) {
+        fence_proxy_async();
+        const unsigned bar = bar0 + 8u * st, dst = stage0 + kStageBytes * st;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "elect.sync _|p, 0xffffffff;\n\t"
+            "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+            "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %1, [%0];\n\t}"
+            ::"r"(bar), "r"(SL::bytes), "r"(dst), "l"(src)
+            : "memory");
+      }
+    } else if (lane == 0 && more) {
+      fence_proxy_async();
+      issue(src, st);
+    }
   };
   if constexpr (PACK && NR == 2) {  // bk padding columns 4*NR.. are the zero rows of the PACK B fragment
     static_assert(WarpSmem<BITS, NR>::kBkRow >= 4 * NR + 4, "PACK zero padding");
@@ -1421,12 +1451,7 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
     __syncwarp();
     // the stage is consumed (codes in registers, params decoded to ws.sz): refill it
     // with block it + kSt (async proxy after generic reads)
-    if (lane == 0) {
-      if (blk + kSt * kWarps < blk1) {
-        fence_proxy_async();
-        issue(next_src, st);
-      }
-    }
+    refill(next_src, st, blk + kSt * kWarps < blk1);
 
     // ---- P.V: B fragments (f16 hi + lo: sum_t P*z and sum_t P*s*code may nearly
     // cancel) and MMAs over 8 channel m-tiles x 2 token k-steps.  PG: one B for
@@ -1583,12 +1608,7 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
     }
     __syncwarp();
     // the stage is consumed: refill it with block it + kSt (async proxy after generic reads)
-    if (lane == 0) {
-      if (blk + kSt * kWarps < blk1) {
-        fence_proxy_async();
-        issue(next_src, st);
-      }
-    }
+    refill(next_src, st, blk + kSt * kWarps < blk1);
 
     // ---- P.V over 8 channel m-tiles x 2 token k-steps -------------------------------------
 #pragma unroll
