@@ -226,3 +226,37 @@ def test_reference_arm_config_matches_gpu_arm():
     a = bench.workload_config(dict(bench.CONFIGS["c3"]), 2, args)
     d = _dry(["--gpus", "2", "--config", "c3", "--dry-run"])
     assert a == d["config"]
+
+
+def test_ctx128k_companion_summary(monkeypatch):
+    """The default single-GPU bench line carries the metric's 128k half: a C3
+    child run whose JSON line is summarised into `ctx_128k` (or the reason it
+    is missing); the child itself is told not to recurse."""
+    import argparse
+    import json
+    import subprocess
+    import bench
+    seen = {}
+    child = {"config": {"workload": "C3: ..."}, "value": 596.0, "unit": "tokens/s", "ms_per_step": 13.4,
+             "steps": 10, "warmup": 3, "e2e": {"value": 611.0},
+             "roofline": {"achieved": 1320.0, "peak": 6500.0, "frac": 0.2, "traffic": 6.6e8,
+                          "avg_launch_ms": 0.41, "kernel_share_of_step": 0.98},
+             "prefetch": {"exposed_fraction": 0.006, "h2d_gbs": 35.5, "h2d_frac": 0.64},
+             "gpu_launches": 1920, "clocks": {"sm_mhz": 1965.0}, "topk_parity": {"band": 1e-4}}
+
+    def fake_run(cmd, **kw):
+        seen["cmd"] = cmd
+        return subprocess.CompletedProcess(cmd, 0, stdout="[log]\n" + json.dumps(child) + "\n", stderr="")
+
+    monkeypatch.setattr(bench.subprocess, "run", fake_run)
+    s = bench.run_ctx128k_companion(argparse.Namespace(steps=10, warmup=3))
+    assert "--no-ctx128k" in seen["cmd"] and seen["cmd"][seen["cmd"].index("--config") + 1] == "c3"
+    assert s["value"] == 596.0 and s["e2e"] == 611.0 and s["roofline"]["frac"] == 0.2
+    assert s["prefetch"]["h2d_frac"] == 0.64 and s["steps"] == 10
+
+    def failing_run(cmd, **kw):
+        return subprocess.CompletedProcess(cmd, 1, stdout="", stderr="CUDA out of memory")
+
+    monkeypatch.setattr(bench.subprocess, "run", failing_run)
+    s = bench.run_ctx128k_companion(argparse.Namespace(steps=10, warmup=3))
+    assert "unavailable" in s and "out of memory" in s["unavailable"]
