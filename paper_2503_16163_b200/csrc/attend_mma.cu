@@ -816,8 +816,11 @@ __device__ void exact_segment_rows(const AttnArgs& a, const int split, const int
   }
 }
 
+#ifndef SPC_K2_TSC
+#define SPC_K2_TSC 1  // 8-row GQA: transposed scores (rows on the MMA M side, P stays in registers)
+#endif
 #ifndef SPC_K2_UWARP_NR
-#define SPC_K2_UWARP_NR 4  // widest row count whose warp index is made uniform (see k_attend_fast)
+#define SPC_K2_UWARP_NR 8  // widest row count whose warp index is made uniform (see k_attend_fast)
 #endif
 #ifndef SPC_K2_GQA_MAXREG
 #define SPC_K2_GQA_MAXREG 0
@@ -869,8 +872,8 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   // warp index through a shuffle: the compiler then treats it (and the block
   // index, ring stage and record address derived from it) as warp-uniform, so
   // the per-block bulk copy takes its operands from uniform registers instead
-  // of a divergent R2UR waterfall loop around UBLKCP.  Not for the 8-row GQA
-  // instantiations: the uniform copies push them over 128 registers (spills).
+  // of a divergent R2UR waterfall loop around UBLKCP.  (The 8-row instantiations
+  // spilled with it before the transposed scores freed their registers.)
   const int warp = NR <= SPC_K2_UWARP_NR ? __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0) : (int)(threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
@@ -937,6 +940,12 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   float Qr[QREG ? NR : 1][4];
   float4* Qs = reinterpret_cast<float4*>(smem_raw + kWarps * sizeof(WarpSmem<BITS, NR>));  // [NR][32]
   constexpr bool HKB = kHalfKeyB && !QREG;
+  // Transposed scores (TSC, 8 rows): D[row hi | row lo][token] = sum_c (Q s)[row][c] code[c][token],
+  // A = the per-block Q*s hi/lo rows (mul_hilo in registers), B = the expanded codes, four n-tiles
+  // of 8 tokens.  A lane then holds row gq's scores of tokens 8nt + 2tq + {0, 1}: exactly the
+  // P.V B-fragment positions, so P never goes through shared memory; the key B table, its
+  // fragment loads and the C_j reduce-scatter disappear too.
+  constexpr bool TSC = SPC_K2_TSC && NR == 8 && HKB && !kCMma && kVCoop;
   // [NR][kQhS] {Qhi b0, Qhi b1, Qlo b0, Qlo b1} (HKB); row stride 36 keeps the C-MMA
   // A-fragment loads (rows gq, gq + 1 in one 8-lane phase) conflict-free
   constexpr int kQhS = 36;
@@ -975,7 +984,7 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
         split2(qq.x * sq, qq.z * sq, h.x, h.z);
         split2(qq.y * sq, qq.w * sq, h.y, h.w);
       }
-      Qh[j * kQhS + lane] = h;
+      Qh[j * kQhS + (TSC ? 4 * kks + ktk : lane)] = h;  // TSC: [row][ks][tq] (conflict-free A loads)
     }
   }
   if (!QREG) __syncthreads();
@@ -998,6 +1007,7 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   // shared memory, the main loop has no register to spare for it
   if (lane == 0) ws.zfold = VCO ? pow2i(Ez - 24 - Ev) : pow2i(-24 - Ev);
   constexpr bool CMM = kCMma && HKB;
+
   // C-MMA: key zero-points as f16 hi + lo of z * 2^-Ezk (max <= 2^14); D * 2^(Ezk + aq) = C_j
   const float rzk = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 4 + 2]);
   const int Ezk = (CMM && rzk > 0.f) ? ceil_log2(rzk) - 14 : 0;
@@ -1022,6 +1032,8 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   }
 
 
+  float* const sprT = (TSC && !a.agg_recompute && gq >= agg_j0 && gq < agg_j0 + G.G)
+                          ? a.spill + ((size_t)b * G.Hq + h * G.G + (gq - agg_j0)) * G.L : nullptr;
   float m_run[RPL], l_run[RPL];
 #pragma unroll
   for (int e = 0; e < RPL; ++e) {
@@ -1109,7 +1121,31 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
 
     // ---- key B fragments (cooperative) + zero-point constants C_j -----------------------
     float Cp[NR];
-    {
+    // TSC tables (in the unused key-B area): [ks][tq] {s hi c0, s hi c1, s lo c0, s lo c1}, then
+    // the zero-points of lane' = (kks, ktk)'s channels 32ktk + kks + 8m
+    uint4* const tst = reinterpret_cast<uint4*>(&ws.bk[0][0]);
+    float4* const tzt = reinterpret_cast<float4*>(&ws.bk[0][0]) + 32;
+    if constexpr (TSC) {
+      const uint4 kp4 = *reinterpret_cast<const uint4*>(S + SL::kp + 4 * lane);
+      const uint32_t kpw[4] = {kp4.x, kp4.y, kp4.z, kp4.w};
+      float s4[4], z4[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const float lo = __uint_as_float(kpw[m] << 16), hi = __uint_as_float(kpw[m] & 0xFFFF0000u);
+        s4[m] = (hi - lo) * kscale;
+        z4[m] = BITS == 1 ? fmaf(0.75f, lo, 0.25f * hi) : lo;
+      }
+      uint32_t sh0, sl0, sh1, sl1;
+      if (BITS == 2) {
+        split2(s4[0], s4[1], sh0, sl0);
+        split2(s4[2], s4[3], sh1, sl1);
+      } else {
+        split2(s4[0], s4[2], sh0, sl0);
+        split2(s4[1], s4[3], sh1, sl1);
+      }
+      tst[4 * kks + ktk] = make_uint4(sh0, sh1, sl0, sl1);
+      tzt[lane] = make_float4(z4[0], z4[1], z4[2], z4[3]);
+    } else {
       const uint4 kp4 = *reinterpret_cast<const uint4*>(S + SL::kp + 4 * lane);
       const uint32_t kpw[4] = {kp4.x, kp4.y, kp4.z, kp4.w};
       float s4[4], z4[4];
@@ -1205,7 +1241,7 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
         for (int o = 16 >> LG; o; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
         Cp[0] = v[0];  // row (lane >> (5 - LG)) of this lane
       }
-    }
+    }  // !TSC
     // value params -> (s * 2^-(q+Ev), z) once per block: lane l decodes words 4l..4l+3
     // (group l>>3, tq (l>>1)&3, ks l&1, slots 0..3; slot>>1 = khalf -> q = 2ks + khalf)
     if constexpr (PG) {
@@ -1271,6 +1307,105 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
       }
       Cp[0] = ((cacc[0] + cacc[1]) + (cacc[2] + cacc[3])) * c_out;  // row gq (valid in lanes tq == 0)
     }
+    float ptsc[TSC ? 4 : 1][2];  // TSC: P of row gq, tokens 8nt + 2tq + {0, 1}
+    if constexpr (TSC) {
+      // C_j of row gq over this lane's quarter of the channels (32tq .. 32tq + 31); the start
+      // is rotated so that the 8 lanes of a shared-memory phase read 8 distinct 16-byte banks
+      float cj = 0.f;
+      {
+        const int rot = tq + 4 * (gq & 1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int kk = (k + rot) & 7;
+          const float4 qq = Qs[gq * 32 + 8 * tq + kk];
+          const float4 zz = tzt[8 * tq + kk];
+          cj = fmaf(qq.x, zz.x, fmaf(qq.y, zz.y, fmaf(qq.z, zz.z, fmaf(qq.w, zz.w, cj))));
+        }
+        cj += __shfl_xor_sync(0xffffffffu, cj, 1);
+        cj += __shfl_xor_sync(0xffffffffu, cj, 2);
+      }
+      float d[4][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const uint4 qh = Qh[gq * kQhS + 4 * ks + tq];  // {Q hi c0, Q hi c1, Q lo c0, Q lo c1} of row gq
+        const uint4 sv = tst[4 * ks + tq];
+        uint32_t a0, a1, a2, a3;  // rows gq (hi) and gq + 8 (lo); K pairs c0 = (2tq, 2tq+1), c1 = (+8, +9)
+        mul_hilo(qh.x, qh.z, sv.x, sv.z, a0, a1);
+        mul_hilo(qh.y, qh.w, sv.y, sv.w, a2, a3);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {  // n-tile 2mt + hf: tokens 16mt + 8hf + (0..7), this lane's gq
+            uint32_t b0, b1;
+            if (BITS == 2) {
+              const uint32_t msk = (3u << (2 * (ks & 3))) | (3u << (16 + 2 * (ks & 3)));
+              const int sh = ks < 4 ? 0 : 8;
+              b0 = (kw[mt][2 * hf] >> sh) & msk;
+              b1 = (kw[mt][2 * hf + 1] >> sh) & msk;
+            } else {
+              const uint32_t msk = (1u << ks) | (1u << (16 + ks));
+              b0 = kw[mt][hf] & msk;
+              b1 = (kw[mt][hf] >> 8) & msk;
+            }
+            mma16816(d[2 * mt + hf], a0, a1, a2, a3, b0, b1);
+          }
+      }
+      // log2 scores of row gq, tokens 8nt + 2tq + e; pins masked; speculative rows spilled
+      float sct[4][2];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) sct[nt][e] = fmaf(d[nt][e] + d[nt][2 + e], k_out, cj);
+      const uint32_t bq2 = bm >> (2 * tq);
+      if (bm) {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if ((bq2 >> (8 * nt + e)) & 1u) sct[nt][e] = -CUDART_INF_F;
+      }
+      if (!kNoSpill && sprT) {
+        float* sp = sprT + blk * 32 + 2 * tq;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (!((bq2 >> (8 * nt + e)) & 1u)) sp[8 * nt + e] = sct[nt][e];
+      }
+      float mloc = fmaxf(fmaxf(sct[0][0], sct[0][1]), fmaxf(sct[1][0], sct[1][1]));
+      mloc = fmaxf(mloc, fmaxf(fmaxf(sct[2][0], sct[2][1]), fmaxf(sct[3][0], sct[3][1])));
+      if (__any_sync(0xffffffffu, mloc > m_run[0] + kSlack)) {
+        float mx = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float mn = fmaxf(m_run[0], mx);
+        const float al = m_run[0] == -CUDART_INF_F ? 0.f : fast_exp2(m_run[0] - mn);
+        l_run[0] *= al;
+        m_run[0] = mn;
+        // value accumulator columns = rows 2tq, 2tq + 1 (their alphas from lanes of those rows)
+        const float ac0 = __shfl_sync(0xffffffffu, al, 8 * tq), ac1 = __shfl_sync(0xffffffffu, al, 8 * tq + 4);
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          dv[mt][0] *= ac0;
+          dv[mt][1] *= ac1;
+          dv[mt][2] *= ac0;
+          dv[mt][3] *= ac1;
+        }
+        zacc[0] *= ac0;
+        zacc[1 % (PG ? 1 : 4)] *= ac1;
+        zacc[2 % (PG ? 1 : 4)] *= ac0;
+        zacc[3 % (PG ? 1 : 4)] *= ac1;
+      }
+      const float mr = m_run[0] == -CUDART_INF_F ? 0.f : m_run[0];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          ptsc[TSC ? nt : 0][e] = fast_exp2(sct[nt][e] - mr);
+          l_run[0] += ptsc[TSC ? nt : 0][e];
+        }
+    } else {
     // ---- scores -------------------------------------------------------------------------
     float dk[2][4], dl[2][4];
 #pragma unroll
@@ -1429,6 +1564,7 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
         }
       }
     }
+    }  // !TSC
     __syncwarp();
 
     if constexpr (PG) {
@@ -1532,8 +1668,13 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
 #pragma unroll
         for (int hf2 = 0; hf2 < 2; ++hf2) {
           const int t = 16 * ks + 2 * tq + 8 * hf2;
-          float2 pp = *reinterpret_cast<const float2*>(&ws.P[WarpSmem<BITS, NR>::pidx(prow, t)]);
-          if (!live) pp = make_float2(0.f, 0.f);
+          float2 pp;
+          if constexpr (TSC) {  // tokens 8 (2ks + hf2) + 2tq + {0, 1} of row gq: this lane's own P
+            pp = make_float2(ptsc[TSC ? 2 * ks + hf2 : 0][0], ptsc[TSC ? 2 * ks + hf2 : 0][1]);
+          } else {
+            pp = *reinterpret_cast<const float2*>(&ws.P[WarpSmem<BITS, NR>::pidx(prow, t)]);
+            if (!live) pp = make_float2(0.f, 0.f);
+          }
           split2(pp.x, pp.y, ph[ks][hf2], pl[ks][hf2]);
         }
       // sum_t P z on the tensor cores: A rows g = z' hi, g + 8 = z' lo of group g (lanes gq < 4;
@@ -1653,8 +1794,13 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
     for (int s = 0; s < kSt; ++s)
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&ws.bar[s])) : "memory");
   }
+  if constexpr (TSC) {  // row gq's sum over its four tq lanes
+    l_run[0] += __shfl_xor_sync(0xffffffffu, l_run[0], 1);
+    l_run[0] += __shfl_xor_sync(0xffffffffu, l_run[0], 2);
+  } else {
 #pragma unroll
-  for (int e = 0; e < RPL; ++e) l_run[e] = warp_sum_g(l_run[e]);
+    for (int e = 0; e < RPL; ++e) l_run[e] = warp_sum_g(l_run[e]);
+  }
   if (VCO) {  // z MMA: D rows gq (z' hi) + gq + 8 (z' lo) of group gq, lanes gq < 4
     zacc[0] += zacc[2 % (PG ? 1 : 4)];
     zacc[1] += zacc[3 % (PG ? 1 : 4)];
@@ -1667,7 +1813,12 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   }
   __syncthreads();
   MergeSmem<NR>& ms = *reinterpret_cast<MergeSmem<NR>*>(smem_raw);
-  if (gq == 0) {
+  if (TSC) {
+    if (tq == 0) {
+      ms.m[warp][gq] = m_run[0];
+      ms.l[warp][gq] = l_run[0];
+    }
+  } else if (gq == 0) {
 #pragma unroll
     for (int e = 0; e < RPL; ++e) {
       if (jr[e] < NR) {
