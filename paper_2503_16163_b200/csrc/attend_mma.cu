@@ -355,7 +355,7 @@ struct ExactRowsSmem {
 
 template <int BITS, int NR>
 constexpr size_t fast_smem_bytes() {
-  size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps + (NR > 2 ? NR * 16 * (32 + (kHalfKeyB ? 36 : 0)) : 0), b = sizeof(MergeSmem<NR>),
+  size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps + (NR > 2 ? NR * 16 * (36 + (kHalfKeyB ? 36 : 0)) : 0), b = sizeof(MergeSmem<NR>),
          c = NR == 8 ? sizeof(ExactRowsSmem<NR>) : sizeof(ExactSmem<NR>);
   return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
@@ -949,7 +949,10 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   // [NR][kQhS] {Qhi b0, Qhi b1, Qlo b0, Qlo b1} (HKB); row stride 36 keeps the C-MMA
   // A-fragment loads (rows gq, gq + 1 in one 8-lane phase) conflict-free
   constexpr int kQhS = 36;
-  uint4* Qh = reinterpret_cast<uint4*>(Qs + NR * 32);
+  uint4* Qh = reinterpret_cast<uint4*>(Qs + NR * 36);
+  // Qs slot of lane' = (kks, ktk)'s channels 32ktk + kks + 8m of row j: TSC reads a row's quarter
+  // tq as [4kk + tq] (stride 36 per row: the 8 lanes of a phase hit 8 distinct 16-byte banks)
+  auto qs_idx = [&](int j, int l) { return TSC ? j * 36 + 4 * (l & 7) + (l >> 3) : j * 32 + l; };
   float qabs = 0.f;
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
@@ -965,7 +968,7 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
 #pragma unroll
       for (int m = 0; m < 4; ++m) Qr[QREG ? j : 0][m] = qv[m];
     } else if (warp == 0) {
-      Qs[j * 32 + lane] = make_float4(qv[0], qv[1], qv[2], qv[3]);
+      Qs[qs_idx(j, lane)] = make_float4(qv[0], qv[1], qv[2], qv[3]);
     }
   }
 #pragma unroll
@@ -975,7 +978,7 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
     const float sq = pow2i(-aq);
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      const float4 qq = Qs[j * 32 + lane];  // written by this lane above
+      const float4 qq = Qs[qs_idx(j, lane)];  // written by this lane above
       uint4 h;
       if (BITS == 2) {  // pairing of the key B fragment: b0 = (m0, m1), b1 = (m2, m3)
         split2(qq.x * sq, qq.y * sq, h.x, h.z);
@@ -1122,7 +1125,7 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
     // ---- key B fragments (cooperative) + zero-point constants C_j -----------------------
     float Cp[NR];
     // TSC tables (in the unused key-B area): [ks][tq] {s hi c0, s hi c1, s lo c0, s lo c1}, then
-    // the zero-points of lane' = (kks, ktk)'s channels 32ktk + kks + 8m
+    // at [4kks + ktk] the zero-points of lane' = (kks, ktk)'s channels 32ktk + kks + 8m
     uint4* const tst = reinterpret_cast<uint4*>(&ws.bk[0][0]);
     float4* const tzt = reinterpret_cast<float4*>(&ws.bk[0][0]) + 32;
     if constexpr (TSC) {
@@ -1144,7 +1147,7 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
         split2(s4[1], s4[3], sh1, sl1);
       }
       tst[4 * kks + ktk] = make_uint4(sh0, sh1, sl0, sl1);
-      tzt[lane] = make_float4(z4[0], z4[1], z4[2], z4[3]);
+      tzt[4 * kks + ktk] = make_float4(z4[0], z4[1], z4[2], z4[3]);
     } else {
       const uint4 kp4 = *reinterpret_cast<const uint4*>(S + SL::kp + 4 * lane);
       const uint32_t kpw[4] = {kp4.x, kp4.y, kp4.z, kp4.w};
@@ -1309,16 +1312,16 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
     }
     float ptsc[TSC ? 4 : 1][2];  // TSC: P of row gq, tokens 8nt + 2tq + {0, 1}
     if constexpr (TSC) {
-      // C_j of row gq over this lane's quarter of the channels (32tq .. 32tq + 31); the start
-      // is rotated so that the 8 lanes of a shared-memory phase read 8 distinct 16-byte banks
+      // C_j of row gq over this lane's quarter of the channels (32tq .. 32tq + 31): tables in
+      // [4kk + tq] order, so the 8 lanes of a shared-memory phase read 8 distinct 16-byte banks
+      // (Qs) or broadcast (z) with immediate offsets
       float cj = 0.f;
       {
-        const int rot = tq + 4 * (gq & 1);
+        const float4* qrow = Qs + gq * 36 + tq;
+        const float4* zrow = tzt + tq;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const int kk = (k + rot) & 7;
-          const float4 qq = Qs[gq * 32 + 8 * tq + kk];
-          const float4 zz = tzt[8 * tq + kk];
+          const float4 qq = qrow[4 * k], zz = zrow[4 * k];
           cj = fmaf(qq.x, zz.x, fmaf(qq.y, zz.y, fmaf(qq.z, zz.z, fmaf(qq.w, zz.w, cj))));
         }
         cj += __shfl_xor_sync(0xffffffffu, cj, 1);
