@@ -1371,11 +1371,17 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
       }
       if (!kNoSpill && sprT) {
         float* sp = sprT + blk * 32 + 2 * tq;
+        if (!(bq2 & 0x03030303u)) {  // no pinned token among this lane's 8: four 8-byte stores
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+          for (int nt = 0; nt < 4; ++nt)
+            *reinterpret_cast<float2*>(sp + 8 * nt) = make_float2(sct[nt][0], sct[nt][1]);
+        } else {
 #pragma unroll
-          for (int e = 0; e < 2; ++e)
-            if (!((bq2 >> (8 * nt + e)) & 1u)) sp[8 * nt + e] = sct[nt][e];
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (!((bq2 >> (8 * nt + e)) & 1u)) sp[8 * nt + e] = sct[nt][e];
+        }
       }
       float mloc = fmaxf(fmaxf(sct[0][0], sct[0][1]), fmaxf(sct[1][0], sct[1][1]));
       mloc = fmaxf(mloc, fmaxf(fmaxf(sct[2][0], sct[2][1]), fmaxf(sct[3][0], sct[3][1])));
