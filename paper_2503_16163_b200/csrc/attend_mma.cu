@@ -355,7 +355,8 @@ struct ExactRowsSmem {
 
 template <int BITS, int NR>
 constexpr size_t fast_smem_bytes() {
-  size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps + (NR > 2 ? NR * 16 * (36 + (kHalfKeyB ? 36 : 0)) : 0), b = sizeof(MergeSmem<NR>),
+  size_t a = sizeof(WarpSmem<BITS, NR>) * kWarps + (NR > 2 ? NR * 16 * (36 + (kHalfKeyB ? 36 : 0)) + 16 : 0),
+         b = sizeof(MergeSmem<NR>),
          c = NR == 8 ? sizeof(ExactRowsSmem<NR>) : sizeof(ExactSmem<NR>);
   return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
@@ -954,8 +955,12 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   // tq as [4kk + tq] (stride 36 per row: the 8 lanes of a phase hit 8 distinct 16-byte banks)
   auto qs_idx = [&](int j, int l) { return TSC ? j * 36 + 4 * (l & 7) + (l >> 3) : j * 32 + l; };
   float qabs = 0.f;
+  // the shared query tables (rows > 2) are loaded by warp 0 alone; the others read its
+  // max |Q| from shared memory after the barrier below
+  float* const qabs_s = reinterpret_cast<float*>(Qh + NR * kQhS);
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
+    if (!QREG && warp != 0) break;
     const int r = j / G.G, g2 = j - r * G.G;
     const __nv_bfloat16* qp = a.q + (((size_t)b * a.rows + r) * G.Hq + h * G.G + g2) * 128;
     float qv[4];
@@ -973,9 +978,10 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) qabs = fmaxf(qabs, __shfl_xor_sync(0xffffffffu, qabs, o));
-  const int aq = (HKB && qabs > 0.f) ? ceil_log2(qabs) - 7 : 0;  // max |Q * 2^-aq| in (2^6, 2^7]
+  if (!QREG && warp == 0 && lane == 0) *qabs_s = qabs;
+  auto aq_of = [&](float qa) { return (HKB && qa > 0.f) ? ceil_log2(qa) - 7 : 0; };  // max |Q * 2^-aq| in (2^6, 2^7]
   if (HKB && warp == 0) {
-    const float sq = pow2i(-aq);
+    const float sq = pow2i(-aq_of(qabs));
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       const float4 qq = Qs[qs_idx(j, lane)];  // written by this lane above
@@ -990,7 +996,11 @@ __global__ void __maxnreg__(k2_maxreg<NR>()) k_attend_fast(AttnArgs a) {
       Qh[j * kQhS + (TSC ? 4 * kks + ktk : lane)] = h;  // TSC: [row][ks][tq] (conflict-free A loads)
     }
   }
-  if (!QREG) __syncthreads();
+  if (!QREG) {
+    __syncthreads();
+    qabs = *qabs_s;  // warp 0's reduction over the shared rows
+  }
+  const int aq = aq_of(qabs);
   const float rk = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 4 + 0]) * cs;
   const float rv = __uint_as_float(B.rmax[((size_t)b * G.H + h) * 4 + 1]) * cs;
   const int Ek = (qabs * rk > 0.f) ? ceil_log2(qabs * rk) - 14 : 0;
