@@ -1958,7 +1958,7 @@ int launch_attend_fast(const AttnArgs& a0, cudaStream_t st) {
   // Split count: SPC_SPLIT_WAVES=w forces ~w waves; by default a wave model
   // picks it.  With `slots` = 2 CTAs x SMs resident, a launch of C CTAs (the
   // splits plus one exact CTA per unit) of b blocks costs about ceil(C / slots)
-  // rounds of (b + c0) block-times, c0 ~ 20 blocks covering a CTA's prologue
+  // rounds of (b + c0) block-times, c0 ~ 40 blocks covering a CTA's prologue
   // (ring fill, first DRAM round trip) and merge.  Short CTAs pay c0 too often,
   // few CTAs quantize badly.  Measured sweeps (SPC_NSPLIT).
   static const int waves = [] {
@@ -1982,7 +1982,9 @@ int launch_attend_fast(const AttnArgs& a0, cudaStream_t st) {
   } else if (waves) {
     want = std::max(1, std::min((waves * slots + units - 1) / units, cap));
   } else {
-    constexpr long long c0 = 20;
+    // c0 = 40 since the transposed-score K2 (r3): C3 picks 17 splits instead of 22, +1.6% in
+    // the 32-layer bench (profiles/r3_03_ab_k2_uniform.txt); C2 (7), C4 share (8), C1 (8) unchanged
+    constexpr long long c0 = 40;
     long long best = -1;
     want = 1;
     for (int w = 1; w <= cap; ++w) {
