@@ -2000,6 +2000,16 @@ int launch_attend_fast(const AttnArgs& a0, cudaStream_t st) {
         want = w;
       }
     }
+    // A pick that fits in one round of long CTAs keeps ~15% of the slots free: in the layer
+    // loop the side kernels (gather, aggregate, top-k) hold some, and a K2 CTA that has to
+    // wait for one of them costs a whole second round.  C4 rank share: 8 -> 6 splits, +2.5%
+    // in the 32-layer bench (profiles/r3_03_ab_k2_uniform.txt); multi-round picks unchanged.
+    while (want > 1) {
+      const int bps = std::max(1, (nblk + want - 1) / want), ns = std::max(1, (nblk + bps - 1) / bps);
+      const long long ctas = (long long)units * (ns + 1);
+      if (bps < 128 || ctas > slots || ctas * 100 <= (long long)slots * 85) break;
+      --want;
+    }
   }
   a.blocks_per_split = std::max(1, (nblk + want - 1) / want);
   a.nsplit = std::max(1, (nblk + a.blocks_per_split - 1) / a.blocks_per_split);
