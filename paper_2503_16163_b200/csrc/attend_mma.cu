@@ -28,6 +28,12 @@
 // construction ("packed groups", PG); otherwise N = rows and each group has
 // its own B fragment.
 //
+// 8 query rows (GQA-4 x {output, speculative}; TSC): the score MMA is transposed, M = rows
+// (hi plane on M rows 0-7, lo plane on 8-15), N = 8 tokens per n-tile, K = channels, with A =
+// the per-block Q*s hi/lo built in registers and B = the expanded codes.  A lane then holds row
+// gq's scores of tokens 8nt + 2tq + {0,1}, which are the P.V B-fragment positions: P stays in
+// registers, and the hi + lo planes of a row sit in one lane.
+//
 // Work split: grid (nsplit + 1, H, batch), 8 warps per CTA.  A CTA streams a
 // contiguous range of 32-token blocks of one (seq, kv head); each warp owns
 // every 8th block and keeps its own online-softmax state; the CTA merges its
