@@ -1991,19 +1991,38 @@ int launch_attend_fast(const AttnArgs& a0, cudaStream_t st) {
     // c0 = 40 since the transposed-score K2 (r3): C3 picks 17 splits instead of 22, +1.6% in
     // the 32-layer bench (profiles/r3_03_ab_k2_uniform.txt); C2 (7), C4 share (8), C1 (8) unchanged
     constexpr long long c0 = 40;
-    long long best = -1;
-    want = 1;
-    for (int w = 1; w <= cap; ++w) {
+    auto cost_of = [&](int w, long long* rounds_out) {
       const int bps = std::max(1, (nblk + w - 1) / w), ns = std::max(1, (nblk + bps - 1) / bps);
       const long long rounds = ((long long)units * (ns + 1) + slots - 1) / slots;  // + the exact CTA
+      if (rounds_out) *rounds_out = rounds;
       // a launch that needs a second round pays ~bps/10 more in the layer loop (its
       // later CTAs start behind the side kernels' CTAs): the C4 rank share's single
       // 8-split wave beats the model's 17-split two rounds by 10% in the bench
       // (profiles/r2_34_*), while C2 (7) and C3 (22) keep their picks
-      const long long cost = rounds * (bps + c0) + (rounds > 1 ? bps / 10 : 0);
+      return rounds * (bps + c0) + (rounds > 1 ? bps / 10 : 0);
+    };
+    long long best = -1, best_rounds = 1;
+    want = 1;
+    for (int w = 1; w <= cap; ++w) {
+      long long rounds;
+      const long long cost = cost_of(w, &rounds);
       if (best < 0 || cost < best) {
         best = cost;
+        best_rounds = rounds;
         want = w;
+      }
+    }
+    // MHA rows (one or two per kv head): of the multi-round picks within 3% of the model's
+    // best, the fewest splits (longest CTAs).  C2: 7 -> 4, +0.9% in the 32-layer bench
+    // (profiles/r3_03_ab_k2_uniform.txt); the model underprices these CTAs' fixed cost
+    if (a.rows * G.G <= 2 && best_rounds > 1) {
+      for (int w = 1; w < want; ++w) {
+        long long rounds;
+        const long long cost = cost_of(w, &rounds);
+        if (rounds > 1 && cost * 100 <= best * 103) {
+          want = w;
+          break;
+        }
       }
     }
     // A pick that fits in one round of long CTAs keeps ~15% of the slots free: in the layer
